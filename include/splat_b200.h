@@ -1,0 +1,139 @@
+/*
+ * splat_b200 — C ABI of the B200 (sm_100a) gradient-aware render + spline
+ * upscale path.  libsplat_b200.so exports exactly the functions below.
+ *
+ * Conventions
+ *  - Every pointer argument is DEVICE memory unless the comment says "host".
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream), performs no host synchronisation and allocates nothing:
+ *    scratch comes from caller-provided workspaces sized by the *_bytes query.
+ *  - Return value: SPLAT_OK or one of the error codes; splat_last_error()
+ *    gives the message (thread-local).  The Python layer maps the codes onto
+ *    the reference exception classes (splinesplat core.py:28-41).
+ *  - Images are row-major HWC float32.  A "gradient image" is the packed
+ *    (H, W, 4, 3) buffer [color, d_dx, d_dy, d_dxdy] plus planar (4, H, W)
+ *    alpha state and an (H, W) int32 contrib_count — the fields of the
+ *    reference GradientImage (raster_forward.py:27-40) in float32.
+ *
+ * Each entry point cites the reference interface it replaces (file:line in
+ * /root/reference/pkg/src/splinesplat).  INTEGRATION.md shows the ctypes
+ * binding.
+ */
+#ifndef SPLAT_B200_H
+#define SPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPLAT_OK 0
+#define SPLAT_ERR_DIMENSION 1   /* DimensionError        (core.py:36) */
+#define SPLAT_ERR_PARAMETER 2   /* ParameterError        (core.py:28) */
+#define SPLAT_ERR_SCALE 3       /* UnsupportedScaleError (core.py:40) */
+#define SPLAT_ERR_CAPACITY 4    /* tile-pair buffer too small: retry larger */
+#define SPLAT_ERR_CUDA 100      /* CUDA runtime error (message in splat_last_error) */
+
+#define SPLAT_ABI_VERSION 1
+
+/* Storage-order scene on the device: the reference Scene arrays
+ * (core.py:75-93) as float64.  n may be 0. */
+typedef struct {
+    int64_t n;
+    const double *means;          /* (n,2) */
+    const double *log_scales;     /* (n,2) */
+    const double *rotations;      /* (n)   */
+    const double *opacity_logits; /* (n)   */
+    const double *colors;         /* (n,3) */
+    const double *depths;         /* (n)   */
+} splat_scene_t;
+
+/* One camera view (host values).  The render of view v at W x H equals the
+ * reference render_forward of Scene(means - (ox, oy), ..., reference_resolution
+ * = (W/kx_ratio...)) with kx = out_w / ref_w, ky = out_h / ref_h exactly as
+ * prepare_scene computes them (raster_forward.py:81-85). */
+typedef struct {
+    double kx, ky;     /* render-resolution scale per axis */
+    double ox, oy;     /* pan, subtracted from means before scaling */
+    double bg[3];      /* background colour (Scene.background) */
+} splat_view_t;
+
+/* Caller-owned outputs of one render (a GradientImage). */
+typedef struct {
+    float *planes;     /* (H,W,4,3) color, d_dx, d_dy, d_dxdy */
+    float *alpha;      /* (4,H,W) alpha, alpha_dx, alpha_dy, alpha_dxdy */
+    int32_t *count;    /* (H,W) contrib_count */
+    uint32_t *last;    /* (H,W) private: tile-list end of the last contributor */
+    double *state;     /* (H,W,4) private float64 terminal (T, A_x, A_y, A_xy); NULL = inference */
+} splat_gimg_t;
+
+/* Pointers into a frame workspace (for inspection / the stage-level API). */
+typedef struct {
+    int16_t *bboxes;        /* (n,4) x0,x1,y0,y1 half-open, rank order (prepare_scene bboxes) */
+    uint32_t *touched;      /* (n) tiles touched per rank, 0 when invalid */
+    uint32_t *offsets;      /* (n+1) exclusive scan of touched */
+    uint32_t *keys;         /* (capacity) sorted tile id per pair */
+    uint32_t *ranks;        /* (capacity) sorted rank per pair */
+    uint32_t *ranges;       /* (ntiles,2) [start,end) into keys/ranks */
+    uint32_t *counters;     /* [0]=pairs [1]=overflow [2]=fix-up pixels [3]=fix-up capacity hit */
+    uint32_t *fixup;        /* (H*W) pixels re-rendered by the exact float64 pass */
+    float *pack;            /* (n,12) float32 per-view pack */
+} splat_frame_ptrs_t;
+
+const char *splat_last_error(void);
+int splat_abi_version(void);
+
+/* ---- per-scene preparation (view independent) --------------------------
+ * Stable depth argsort (raster_forward.py:59-61) and the view-independent
+ * float64 terms of prepare_scene (raster_forward.py:86-110): e^{-2l}, cos,
+ * sin, sigma = logistic(logit), q = log(max(sigma*255,1)), n00/n01/n11, e1*e2. */
+size_t splat_scene_const_bytes(int64_t n);
+size_t splat_scene_workspace_bytes(int64_t n);
+int splat_scene_prepare(const splat_scene_t *scene, void *const_buf, size_t const_bytes,
+                        void *workspace, size_t ws_bytes, void *stream);
+/* rank -> storage index (int32, n) inside const_buf (sort_by_depth output) */
+const int32_t *splat_scene_order(const void *const_buf, int64_t n);
+
+/* ---- per-view render with analytic gradients ---------------------------
+ * render_forward (raster_forward.py:152-187): preprocess (prepare_scene),
+ * tile binning with a device radix sort (bin_tiles), the 16x16-tile
+ * front-to-back rasterizer (_kernels.forward_region, _kernels.py:32-129) and
+ * an exact float64 re-render of pixels whose termination decision was too
+ * close to call in float32.  train != 0 also writes the private float64
+ * terminal state needed by splat_render_backward. */
+size_t splat_frame_workspace_bytes(int64_t n, int width, int height, int64_t pair_capacity);
+int splat_frame_pointers(void *workspace, int64_t n, int width, int height, int64_t pair_capacity,
+                         splat_frame_ptrs_t *out /* host */);
+int splat_render_forward(const void *scene_const, int64_t n, const splat_view_t *view /* host */,
+                         int width, int height, int train, const splat_gimg_t *out /* host struct */,
+                         void *workspace, size_t ws_bytes, int64_t pair_capacity, void *stream);
+/* Stage-level entry points (inspection; the fused call above runs them all). */
+int splat_prepare_view(const void *scene_const, int64_t n, const splat_view_t *view, int width,
+                       int height, void *workspace, size_t ws_bytes, int64_t pair_capacity,
+                       void *stream);
+int splat_bin_tiles(int64_t n, int width, int height, void *workspace, size_t ws_bytes,
+                    int64_t pair_capacity, void *stream);
+/* Exact float64 RenderPack of a view (prepare_scene means/conics/sigmas,
+ * raster_forward.py:86-102), rank order: pack64 (n,6) = mx,my,a,b,c,sigma;
+ * colors64 (n,3) may be NULL.  Inspection only (the rasterizer uses float32). */
+int splat_view_pack64(const void *scene_const, int64_t n, const splat_view_t *view, double *pack64,
+                      void *stream);
+
+/* ---- spline upscaler ----------------------------------------------------
+ * upscale_spline (spline.py:162-178): (H,W,4,3) gradient planes -> (Ho,Wo,3).
+ * upscale_backward (spline.py:191-243): (Ho,Wo,3) adjoint -> (H,W,4,3). */
+int splat_upscale_forward(const float *src, int in_w, int in_h, float *out, int out_w, int out_h,
+                          int clamp, void *stream);
+int splat_upscale_backward(const float *adjoint, int out_w, int out_h, float *dsrc, int in_w,
+                           int in_h, void *stream);
+/* fd_gradients / fd_gradients_backward (spline.py:274-297). */
+int splat_fd_gradients(const float *image, int width, int height, float *planes, void *stream);
+int splat_fd_gradients_backward(const float *dplanes, int width, int height, float *dimage,
+                                float *scratch /* (H,W,3) */, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLAT_B200_H */

@@ -1,0 +1,157 @@
+// extern "C" boundary of libsplat_b200.so (declared in include/splat_b200.h).
+#include <cstdio>
+#include <cstring>
+
+#include "kernels.cuh"
+
+namespace splat {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* msg) {
+    std::snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* what) {
+    std::snprintf(g_err, sizeof(g_err), "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    return SPLAT_ERR_CUDA;
+}
+
+size_t scene_workspace_bytes_impl(int64_t n);
+int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaStream_t stream);
+bool sorted_in_alt(int ntiles);
+int launch_pack64(const SceneConst& sc, const ViewConst& vc, double* out, cudaStream_t stream);
+int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
+                         int clamp, cudaStream_t stream);
+int upscale_backward_impl(const float* adj, int out_w, int out_h, float* dsrc, int in_w, int in_h,
+                          cudaStream_t stream);
+int fd_forward_impl(const float* img, int w, int h, float* planes, cudaStream_t stream);
+int fd_backward_impl(const float* dplanes, int w, int h, float* tmp, float* out, cudaStream_t stream);
+
+static int check_dims(int width, int height) {
+    if (width <= 0 || height <= 0)
+        return set_error(SPLAT_ERR_DIMENSION, "output dimensions must be positive");
+    if (width > 32767 || height > 32767)
+        return set_error(SPLAT_ERR_DIMENSION, "render dimensions above 32767 are not supported");
+    return SPLAT_OK;
+}
+
+}  // namespace splat
+
+using namespace splat;
+
+extern "C" {
+
+const char* splat_last_error(void) { return g_err; }
+int splat_abi_version(void) { return SPLAT_ABI_VERSION; }
+
+size_t splat_scene_const_bytes(int64_t n) { return const_layout(n).total; }
+size_t splat_scene_workspace_bytes(int64_t n) { return scene_workspace_bytes_impl(n); }
+
+int splat_scene_prepare(const splat_scene_t* scene, void* const_buf, size_t const_bytes, void* workspace,
+                        size_t ws_bytes, void* stream) {
+    if (!scene || scene->n < 0) return set_error(SPLAT_ERR_PARAMETER, "invalid scene");
+    if (scene->n >= (int64_t)1 << 31) return set_error(SPLAT_ERR_PARAMETER, "too many splats");
+    if (const_bytes < const_layout(scene->n).total || ws_bytes < scene_workspace_bytes_impl(scene->n))
+        return set_error(SPLAT_ERR_PARAMETER, "scene buffers too small");
+    return scene_prepare_impl(*scene, const_buf, workspace, (cudaStream_t)stream);
+}
+
+const int32_t* splat_scene_order(const void* const_buf, int64_t n) {
+    return scene_const_view(const_buf, n).order;
+}
+
+size_t splat_frame_workspace_bytes(int64_t n, int width, int height, int64_t pair_capacity) {
+    return frame_layout(n, width, height, pair_capacity).total;
+}
+
+int splat_frame_pointers(void* workspace, int64_t n, int width, int height, int64_t pair_capacity,
+                         splat_frame_ptrs_t* out) {
+    FrameLayout L = frame_layout(n, width, height, pair_capacity);
+    char* w = (char*)workspace;
+    bool alt = sorted_in_alt(L.ntx * L.nty);
+    out->bboxes = (int16_t*)(w + L.bboxes);
+    out->touched = (uint32_t*)(w + L.touched);
+    out->offsets = (uint32_t*)(w + L.offsets);
+    out->keys = (uint32_t*)(w + (alt ? L.keys1 : L.keys0));
+    out->ranks = (uint32_t*)(w + (alt ? L.vals1 : L.vals0));
+    out->ranges = (uint32_t*)(w + L.ranges);
+    out->counters = (uint32_t*)(w + L.counters);
+    out->fixup = (uint32_t*)(w + L.fixup);
+    out->pack = (float*)(w + L.pack);
+    return SPLAT_OK;
+}
+
+int splat_prepare_view(const void* scene_const, int64_t n, const splat_view_t* view, int width,
+                       int height, void* workspace, size_t ws_bytes, int64_t pair_capacity, void* stream) {
+    int rc = check_dims(width, height);
+    if (rc) return rc;
+    FrameLayout L = frame_layout(n, width, height, pair_capacity);
+    if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    return launch_preprocess(scene_const_view(scene_const, n), make_view_const(*view), L, (char*)workspace,
+                             (cudaStream_t)stream);
+}
+
+int splat_bin_tiles(int64_t n, int width, int height, void* workspace, size_t ws_bytes,
+                    int64_t pair_capacity, void* stream) {
+    int rc = check_dims(width, height);
+    if (rc) return rc;
+    FrameLayout L = frame_layout(n, width, height, pair_capacity);
+    if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    return launch_binning(L, (char*)workspace, (cudaStream_t)stream);
+}
+
+int splat_view_pack64(const void* scene_const, int64_t n, const splat_view_t* view, double* pack64,
+                      void* stream) {
+    return launch_pack64(scene_const_view(scene_const, n), make_view_const(*view), pack64,
+                         (cudaStream_t)stream);
+}
+
+int splat_render_forward(const void* scene_const, int64_t n, const splat_view_t* view, int width, int height,
+                         int train, const splat_gimg_t* out, void* workspace, size_t ws_bytes,
+                         int64_t pair_capacity, void* stream) {
+    int rc = check_dims(width, height);
+    if (rc) return rc;
+    if (train && !out->state) return set_error(SPLAT_ERR_PARAMETER, "train mode needs the state buffer");
+    FrameLayout L = frame_layout(n, width, height, pair_capacity);
+    if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    SceneConst sc = scene_const_view(scene_const, n);
+    ViewConst vc = make_view_const(*view);
+    char* w = (char*)workspace;
+    if ((rc = launch_preprocess(sc, vc, L, w, s))) return rc;
+    if ((rc = launch_binning(L, w, s))) return rc;
+    return launch_raster_forward(sc, vc, L, w, *out, train != 0, s);
+}
+
+int splat_upscale_forward(const float* src, int in_w, int in_h, float* out, int out_w, int out_h, int clamp,
+                          void* stream) {
+    if (in_w <= 0 || in_h <= 0) return set_error(SPLAT_ERR_DIMENSION, "empty source image");
+    if (out_w < in_w || out_h < in_h)
+        return set_error(SPLAT_ERR_SCALE, "output must be at least source size");
+    return upscale_forward_impl(src, in_w, in_h, out, out_w, out_h, clamp, (cudaStream_t)stream);
+}
+
+int splat_upscale_backward(const float* adjoint, int out_w, int out_h, float* dsrc, int in_w, int in_h,
+                           void* stream) {
+    if (in_w <= 0 || in_h <= 0) return set_error(SPLAT_ERR_DIMENSION, "empty source image");
+    if (out_w < in_w || out_h < in_h)
+        return set_error(SPLAT_ERR_SCALE, "output must be at least source size");
+    return upscale_backward_impl(adjoint, out_w, out_h, dsrc, in_w, in_h, (cudaStream_t)stream);
+}
+
+int splat_fd_gradients(const float* image, int width, int height, float* planes, void* stream) {
+    if (width < 2 || height < 2)
+        return set_error(SPLAT_ERR_DIMENSION, "finite differences need at least 2x2 pixels");
+    return fd_forward_impl(image, width, height, planes, (cudaStream_t)stream);
+}
+
+int splat_fd_gradients_backward(const float* dplanes, int width, int height, float* dimage,
+                                float* scratch, void* stream) {
+    if (width < 2 || height < 2)
+        return set_error(SPLAT_ERR_DIMENSION, "finite differences need at least 2x2 pixels");
+    return fd_backward_impl(dplanes, width, height, scratch, dimage, (cudaStream_t)stream);
+}
+
+}  // extern "C"

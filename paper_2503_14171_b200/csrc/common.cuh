@@ -1,0 +1,53 @@
+// Shared definitions for the sm_100a render + upscale kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/splat_b200.h"
+
+namespace splat {
+
+constexpr int kTile = 16;                 // raster_forward.py:24
+constexpr int kBlock = 256;               // one 16x16 tile per CTA
+constexpr double kAlphaClamp = 0.999;     // core.py:23
+constexpr double kAlphaCull = 1.0 / 255.0;  // core.py:24
+constexpr double kEarlyTerm = 1e-4;       // core.py:25
+// _kernels.py:29 LOG_CULL = float(np.log(1/255)); bit pattern taken from numpy.
+constexpr double kLogCull = -5.541263545158426;
+
+// Rank-ordered, view-independent per-splat constants (computed once per scene
+// on the device).  Struct-of-arrays, float64 unless noted.
+struct SceneConst {
+    int64_t n;
+    const int32_t* order;   // rank -> storage index (stable depth argsort)
+    const double* mean;     // (n,2) means gathered into rank order
+    const double* n00;      // e1 c^2 + e2 s^2          (raster_forward.py:96)
+    const double* n01;      // (e1 - e2) s c            (raster_forward.py:97)
+    const double* n11;      // e1 s^2 + e2 c^2          (raster_forward.py:98)
+    const double* e1e2;     // e1 * e2                  (raster_forward.py:108)
+    const double* sigma;    // logistic(opacity_logit)  (raster_forward.py:89)
+    const double* q;        // log(max(sigma/(1/255),1)) (raster_forward.py:107)
+    const float4* color;    // (n) float32 rgb_ colours in rank order
+};
+
+// Per-view float32 pack the rasterizer consumes (rank order, 48 bytes).
+struct __align__(16) PackF {
+    float mxh, mxl, myh, myl;     // render-space mean as float hi + lo parts
+    float a, b, c, sigma;         // conic and opacity
+    float qcull, qclamp, pad0, pad1;  // ln(255 sigma), ln(sigma / 0.999)
+};
+
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace splat
+
+#define SPLAT_CUDA_CHECK(expr)                                   \
+    do {                                                         \
+        cudaError_t _e = (expr);                                 \
+        if (_e != cudaSuccess) return splat::set_cuda_error(_e, #expr); \
+    } while (0)
+
+namespace splat {
+int set_cuda_error(cudaError_t e, const char* what);
+int set_error(int code, const char* msg);
+}  // namespace splat

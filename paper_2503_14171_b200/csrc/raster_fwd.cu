@@ -1,0 +1,456 @@
+// Front-to-back gradient rasterizer (forward) for sm_100a.
+//
+// Semantics: _kernels.forward_region (_kernels.py:32-129) per pixel, on the
+// 16x16 tile lists of bin_tiles.  One CTA per tile, 8 warps, each warp owns an
+// 8x4 pixel rectangle (one pixel per lane).  Candidates are staged in shared
+// memory 256 at a time together with an 8-bit mask of the warp rectangles
+// their bbox touches; a warp walks only the candidates whose mask bit is set
+// (warp-level bbox rejection) and leaves as soon as all its pixels terminated
+// (warp-level early termination).
+//
+// Precision design: every blending decision of the reference
+// — cull (alpha < 1/255), clamp (alpha > 0.999) and early termination
+// (1 - A < 1e-4) — is decided in float32 with a rigorous error bound; a
+// candidate whose cull/clamp test falls inside the bound is re-evaluated with
+// the reference's exact float64 arithmetic, and a pixel whose termination test
+// falls inside the bound is re-rendered by `fixup_kernel` with the exact
+// float64 blend chain.  The decisions (hence contrib_count and every per-tile
+// contributor list) therefore equal the reference's; values are float32.
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace splat {
+
+namespace {
+
+enum : int { kCulled = 0, kContrib = 1, kClamped = 2, kUnsure = 3 };
+
+struct RasterArgs {
+    SceneConst sc;
+    ViewConst vc;
+    int width, height, ntx;
+    const uint32_t* ranges;
+    const uint32_t* ranks;
+    const PackF* pack;
+    const short4* bboxes;
+    float* planes;
+    float* alpha;
+    int32_t* count;
+    uint32_t* last;
+    double* state;
+    uint32_t* fixup;
+    uint32_t* counters;
+};
+
+// Exact reference evaluation of one candidate at one pixel centre
+// (_kernels.py:61-80, float64, every operation individually rounded).
+__device__ __noinline__ int eval_exact(const SceneConst& sc, const ViewConst& vc, const short4* bboxes,
+                                       uint32_t r, int px, int py, double* alpha64) {
+    short4 bb = bboxes[r];
+    if (px < bb.x || px >= bb.y || py < bb.z || py >= bb.w) return kCulled;
+    double mx = __dmul_rn(__dsub_rn(sc.mean[2 * r], vc.ox), vc.kx);
+    double my = __dmul_rn(__dsub_rn(sc.mean[2 * r + 1], vc.oy), vc.ky);
+    double ca = __ddiv_rn(sc.n00[r], vc.c00);
+    double cb = __ddiv_rn(sc.n01[r], vc.c01);
+    double cc = __ddiv_rn(sc.n11[r], vc.c11);
+    double dx = __dsub_rn((double)px + 0.5, mx);
+    double dy = __dsub_rn((double)py + 0.5, my);
+    double t1 = __dmul_rn(__dmul_rn(ca, dx), dx);
+    double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, cb), dx), dy);
+    double t3 = __dmul_rn(__dmul_rn(cc, dy), dy);
+    double expo = -__dadd_rn(__dadd_rn(t1, t2), t3);
+    if (expo < kLogCull) return kCulled;
+    double araw = __dmul_rn(sc.sigma[r], exp(expo));
+    if (araw < kAlphaCull) return kCulled;
+    if (araw > kAlphaClamp) {
+        *alpha64 = kAlphaClamp;
+        return kClamped;
+    }
+    *alpha64 = araw;
+    return kContrib;
+}
+
+// Float32 footprint with a certified decision (_kernels.py:65-87).  Returns
+// kCulled / kContrib / kClamped when the float32 evaluation decides the
+// reference's tests with margin, kUnsure otherwise.  `al` etc. are the
+// canonical float32 values used for blending (identical in the backward pass);
+// `rel` receives the relative error bound of `al`.
+__device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, float& al, float& ax,
+                                         float& ay, float& axy, float& rel) {
+    float dx = (cx - g.mxh) - g.mxl;
+    float dy = (cy - g.myh) - g.myl;
+    float adx = g.a * dx;
+    float b2 = 2.f * g.b;
+    float t1 = adx * dx;
+    float t2 = (b2 * dx) * dy;
+    float t3 = (g.c * dy) * dy;
+    float qf = (t1 + t2) + t3;
+    float s = (t1 + fabsf(t2)) + t3;
+    // |qf - Q_exact| <= ~8 ulp * s; conic/mean rounding adds ~4 ulp * s.  2^-19 * s is a 2x margin.
+    float tol = fmaf(s + g.qcull, 1.9073486e-06f, 1e-30f);
+    rel = fmaf(s, 4.7683716e-07f, 1.9073486e-06f);  // |al - alpha_ref| / al <= 2^-21 s + 2^-19
+    if (qf > g.qcull + tol) return kCulled;
+    if (qf >= g.qcull - tol) return kUnsure;
+    if (qf <= g.qclamp + tol) {
+        if (qf < g.qclamp - tol) {
+            al = 0.999f;
+            ax = 0.f;
+            ay = 0.f;
+            axy = 0.f;
+            return kClamped;
+        }
+        return kUnsure;
+    }
+    float e = __expf(-qf);
+    al = g.sigma * e;
+    float gx = -2.f * fmaf(g.b, dy, adx);
+    float gy = -2.f * fmaf(g.b, dx, g.c * dy);
+    ax = al * gx;
+    ay = al * gy;
+    axy = al * fmaf(gx, gy, -b2);
+    return kContrib;
+}
+
+// Values of a candidate whose decision came from the exact path.
+__device__ __forceinline__ void canonical_values(const PackF& g, float cx, float cy, int st, float& al,
+                                                 float& ax, float& ay, float& axy) {
+    if (st == kClamped) {
+        al = 0.999f;
+        ax = ay = axy = 0.f;
+        return;
+    }
+    float dx = (cx - g.mxh) - g.mxl;
+    float dy = (cy - g.myh) - g.myl;
+    float adx = g.a * dx;
+    float b2 = 2.f * g.b;
+    float qf = ((adx * dx) + ((b2 * dx) * dy)) + ((g.c * dy) * dy);
+    al = g.sigma * __expf(-qf);
+    float gx = -2.f * fmaf(g.b, dy, adx);
+    float gy = -2.f * fmaf(g.b, dx, g.c * dy);
+    ax = al * gx;
+    ay = al * gy;
+    axy = al * fmaf(gx, gy, -b2);
+}
+
+// Per-pixel blend state (_kernels.py:41-57 accumulators).  T is the
+// transmittance 1 - A; TRAIN keeps the A-state in float64 for the backward
+// inversion.
+template <bool TRAIN>
+struct Blend {
+    float b[3], bx[3], by[3], bxy[3];
+    float T, ax, ay, axy;          // float32 state (inference)
+    double Td, axd, ayd, axyd;     // float64 state (training)
+    float eps;                     // relative error bound of T
+    int n;
+    uint32_t last;
+
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) b[c] = bx[c] = by[c] = bxy[c] = 0.f;
+        T = 1.f;
+        ax = ay = axy = 0.f;
+        Td = 1.0;
+        axd = ayd = axyd = 0.0;
+        eps = 0.f;
+        n = 0;
+        last = 0;
+    }
+
+    // One contributor (_kernels.py:88-109).  om = 1 - alpha (exactly 1e-3 when clamped).
+    __device__ __forceinline__ void add(float al, float gax, float gay, float gaxy, float om,
+                                        const float4& col) {
+        float t, sx, sy, sxy;
+        if (TRAIN) {
+            t = (float)Td;
+            sx = (float)axd;
+            sy = (float)ayd;
+            sxy = (float)axyd;
+        } else {
+            t = T;
+            sx = ax;
+            sy = ay;
+            sxy = axy;
+        }
+        float tx_ = t * gax - sx * al;
+        float ty_ = t * gay - sy * al;
+        float txy = ((t * gaxy - sy * gax) - sxy * al) - sx * gay;
+        float ta = t * al;
+        float cc[3] = {col.x, col.y, col.z};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            bx[c] = fmaf(cc[c], tx_, bx[c]);
+            by[c] = fmaf(cc[c], ty_, by[c]);
+            bxy[c] = fmaf(cc[c], txy, bxy[c]);
+            b[c] = fmaf(cc[c], ta, b[c]);
+        }
+        if (TRAIN) {
+            double a = al, gx = gax, gy = gay, gxy = gaxy, o = om;
+            double nx = fma(axd, o, Td * gx);
+            double ny = fma(ayd, o, Td * gy);
+            double nxy = fma(axyd, o, Td * gxy) - axd * gy - ayd * gx;
+            (void)a;
+            axd = nx;
+            ayd = ny;
+            axyd = nxy;
+            Td = Td * o;
+            T = (float)Td;
+        } else {
+            float nx = fmaf(ax, om, t * gax);
+            float ny = fmaf(ay, om, t * gay);
+            float nxy = (fmaf(axy, om, t * gaxy) - ax * gay) - ay * gax;
+            ax = nx;
+            ay = ny;
+            axy = nxy;
+            T = T * om;
+        }
+        ++n;
+    }
+};
+
+__device__ __forceinline__ uint8_t warp_mask_of(short4 bb, int tx0, int ty0) {
+    // bit (row*2 + col): warp rectangle col in {0,1} (8 px), row in {0..3} (4 px)
+    uint32_t cols = 0, rows = 0;
+    if (bb.x < tx0 + 8 && bb.y > tx0) cols |= 1u;
+    if (bb.x < tx0 + 16 && bb.y > tx0 + 8) cols |= 2u;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (bb.z < ty0 + 4 * (r + 1) && bb.w > ty0 + 4 * r) rows |= 1u << r;
+    uint32_t m = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (rows & (1u << r)) m |= cols << (2 * r);
+    return (uint8_t)m;
+}
+
+template <bool TRAIN>
+__device__ __forceinline__ void write_pixel(const RasterArgs& p, int px, int py, const Blend<TRAIN>& s) {
+    int64_t o = (int64_t)py * p.width + px;
+    float bgc[3] = {p.vc.bg[0], p.vc.bg[1], p.vc.bg[2]};
+    float T = s.T, sx, sy, sxy;
+    if (TRAIN) {
+        sx = (float)s.axd;
+        sy = (float)s.ayd;
+        sxy = (float)s.axyd;
+    } else {
+        sx = s.ax;
+        sy = s.ay;
+        sxy = s.axy;
+    }
+    float v[12];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        v[c] = fmaf(T, bgc[c], s.b[c]);          // _kernels.py:112-115
+        v[3 + c] = s.bx[c] - sx * bgc[c];        // _kernels.py:116-118
+        v[6 + c] = s.by[c] - sy * bgc[c];
+        v[9 + c] = s.bxy[c] - sxy * bgc[c];
+    }
+    float4* dst = reinterpret_cast<float4*>(p.planes + 12 * o);
+    dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+    dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+    dst[2] = make_float4(v[8], v[9], v[10], v[11]);
+    int64_t P = (int64_t)p.width * p.height;
+    p.alpha[o] = TRAIN ? (float)(1.0 - s.Td) : 1.f - T;
+    p.alpha[P + o] = sx;
+    p.alpha[2 * P + o] = sy;
+    p.alpha[3 * P + o] = sxy;
+    p.count[o] = s.n;
+    p.last[o] = s.last;
+    if (TRAIN) {
+        double2* st = reinterpret_cast<double2*>(p.state + 4 * o);
+        st[0] = make_double2(s.Td, s.axd);
+        st[1] = make_double2(s.ayd, s.axyd);
+    }
+}
+
+constexpr float kTermF = 1e-4f;
+
+template <bool TRAIN>
+__global__ void __launch_bounds__(kBlock) raster_fwd_kernel(RasterArgs p) {
+    __shared__ PackF s_pack[kBlock];
+    __shared__ float4 s_col[kBlock];
+    __shared__ uint32_t s_rank[kBlock];
+    __shared__ uint8_t s_mask[kBlock];
+
+    const int tile = blockIdx.x;
+    const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tx0 = tile_x * kTile, ty0 = tile_y * kTile;
+    const int px = tx0 + (warp & 1) * 8 + (lane & 7);
+    const int py = ty0 + (warp >> 1) * 4 + (lane >> 3);
+    const bool inside = px < p.width && py < p.height;
+    const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
+    const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
+
+    Blend<TRAIN> s;
+    s.init();
+    s.last = start;
+    bool active = inside;
+    bool flagged = false;
+
+    for (uint32_t base = start; base < end; base += kBlock) {
+        if (__syncthreads_count(active) == 0) break;
+        uint32_t j = base + tid;
+        uint8_t m = 0;
+        if (j < end) {
+            uint32_t r = p.ranks[j];
+            short4 bb = p.bboxes[r];
+            m = warp_mask_of(bb, tx0, ty0);
+            s_pack[tid] = p.pack[r];
+            s_col[tid] = p.sc.color[r];
+            s_rank[tid] = r;
+        }
+        s_mask[tid] = m;
+        __syncthreads();
+        const int nb = (int)min((uint32_t)kBlock, end - base);
+        if (__any_sync(0xffffffffu, active)) {
+            for (int chunk = 0; chunk < nb; chunk += 32) {
+                uint32_t bits = __ballot_sync(0xffffffffu, (s_mask[chunk + lane] >> warp) & 1u);
+                while (bits) {
+                    const int k = chunk + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    if (active) {
+                        const PackF g = s_pack[k];
+                        float al, gax, gay, gaxy, rel = 0.f;
+                        int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
+                        if (st == kUnsure) {
+                            double a64;
+                            st = eval_exact(p.sc, p.vc, p.bboxes, s_rank[k], px, py, &a64);
+                            if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
+                        }
+                        if (st != kCulled) {
+                            float om = st == kClamped ? 1.0e-3f : 1.f - al;
+                            if (st == kClamped) rel = 0.f;
+                            s.add(al, gax, gay, gaxy, om, s_col[k]);
+                            s.last = base + k + 1;
+                            // relative error of om, plus one rounding of the product
+                            s.eps += fmaf(__fdividef(al, om), rel, 1.2e-7f);
+                            float T = s.T;
+                            float m_ = fmaf(4.f, s.eps, 2e-6f);
+                            if (T < kTermF * (1.f - m_)) {
+                                active = false;  // certainly terminated (_kernels.py:110-111)
+                            } else if (T <= kTermF * (1.f + m_)) {
+                                active = false;  // too close to call: exact re-render
+                                flagged = true;
+                            }
+                        }
+                    }
+                    if (!__any_sync(0xffffffffu, active)) break;
+                }
+                if (!__any_sync(0xffffffffu, active)) break;
+            }
+        }
+    }
+    if (inside) {
+        write_pixel<TRAIN>(p, px, py, s);
+        if (flagged) {
+            uint32_t slot = atomicAdd(&p.counters[2], 1u);
+            p.fixup[slot] = (uint32_t)(py * p.width + px);
+        }
+    }
+}
+
+// Exact re-render of flagged pixels: one warp per pixel.  Lanes evaluate 32
+// candidates at a time with the exact float64 test, then the warp walks the
+// contributors in order, running the reference's float64 accumulation
+// `acc = acc + alpha * (1 - acc)` for the termination decision and the usual
+// float32 (or TRAIN float64) value recurrences for the outputs.
+template <bool TRAIN>
+__global__ void __launch_bounds__(256) fixup_kernel(RasterArgs p) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nfix = p.counters[2];
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nfix;
+         w += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t pix = p.fixup[w];
+        const int px = (int)(pix % (uint32_t)p.width), py = (int)(pix / (uint32_t)p.width);
+        const int tile = (py / kTile) * p.ntx + px / kTile;
+        const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
+        const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
+        Blend<TRAIN> s;
+        s.init();
+        s.last = start;
+        double acc = 0.0;
+        bool done = false;
+        for (uint32_t base = start; base < end && !done; base += 32) {
+            uint32_t j = base + lane;
+            int st = kCulled;
+            double a64 = 0.0;
+            uint32_t r = 0;
+            if (j < end) {
+                r = p.ranks[j];
+                st = eval_exact(p.sc, p.vc, p.bboxes, r, px, py, &a64);
+            }
+            float al = 0.f, gax = 0.f, gay = 0.f, gaxy = 0.f;
+            float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (st != kCulled) {
+                const PackF g = p.pack[r];
+                canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
+                col = p.sc.color[r];
+            }
+            uint32_t bits = __ballot_sync(0xffffffffu, st != kCulled);
+            while (bits) {
+                const int k = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const double ak = __shfl_sync(0xffffffffu, a64, k);
+                const int stk = __shfl_sync(0xffffffffu, st, k);
+                const float alk = __shfl_sync(0xffffffffu, al, k);
+                const float axk = __shfl_sync(0xffffffffu, gax, k);
+                const float ayk = __shfl_sync(0xffffffffu, gay, k);
+                const float axyk = __shfl_sync(0xffffffffu, gaxy, k);
+                float4 ck;
+                ck.x = __shfl_sync(0xffffffffu, col.x, k);
+                ck.y = __shfl_sync(0xffffffffu, col.y, k);
+                ck.z = __shfl_sync(0xffffffffu, col.z, k);
+                ck.w = 0.f;
+                const float om = stk == kClamped ? 1.0e-3f : 1.f - alk;
+                s.add(alk, axk, ayk, axyk, om, ck);
+                s.last = base + k + 1;
+                // reference accumulation and test (_kernels.py:105-111)
+                double t = __dsub_rn(1.0, acc);
+                acc = __dadd_rn(acc, __dmul_rn(ak, t));
+                if (__dsub_rn(1.0, acc) < kEarlyTerm) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+        if (lane == 0) write_pixel<TRAIN>(p, px, py, s);
+    }
+}
+
+}  // namespace
+
+int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
+                          const splat_gimg_t& out, bool train, cudaStream_t stream) {
+    RasterArgs a;
+    a.sc = sc;
+    a.vc = vc;
+    a.width = L.width;
+    a.height = L.height;
+    a.ntx = L.ntx;
+    a.ranges = (const uint32_t*)(ws + L.ranges);
+    extern bool sorted_in_alt(int ntiles);
+    bool alt = sorted_in_alt(L.ntx * L.nty);
+    a.ranks = (const uint32_t*)(ws + (alt ? L.vals1 : L.vals0));
+    a.pack = (const PackF*)(ws + L.pack);
+    a.bboxes = (const short4*)(ws + L.bboxes);
+    a.planes = out.planes;
+    a.alpha = out.alpha;
+    a.count = out.count;
+    a.last = out.last;
+    a.state = out.state;
+    a.fixup = (uint32_t*)(ws + L.fixup);
+    a.counters = (uint32_t*)(ws + L.counters);
+    int ntiles = L.ntx * L.nty;
+    if (train) {
+        raster_fwd_kernel<true><<<ntiles, kBlock, 0, stream>>>(a);
+        fixup_kernel<true><<<148 * 2, 256, 0, stream>>>(a);
+    } else {
+        raster_fwd_kernel<false><<<ntiles, kBlock, 0, stream>>>(a);
+        fixup_kernel<false><<<148 * 2, 256, 0, stream>>>(a);
+    }
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
+
+}  // namespace splat

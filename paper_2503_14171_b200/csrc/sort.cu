@@ -1,0 +1,236 @@
+// Device primitives for tile binning: exclusive scan and a stable LSD radix
+// sort of (key, value) pairs.  Hand-written for sm_100a (no CUB): the binning
+// pass only needs the tile-id bits sorted, because pairs are emitted in rank
+// order and the sort is stable (raster_forward.py:136-149 appends ranks to each
+// tile list in ascending order).
+#include "kernels.cuh"
+
+namespace splat {
+
+namespace {
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;                       // per thread
+constexpr int kScanTile = kScanThreads * kScanItems;  // 4096 per block
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t o = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += o;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one value per thread (1024 threads).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = warp_incl_scan(v, lane);
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = s_warp[lane];
+        uint32_t wi = warp_incl_scan(w, lane);
+        s_warp[lane] = wi - w;
+        if (lane == 31) s_warp[32] = wi;
+    }
+    __syncthreads();
+    uint32_t r = s_warp[warp] + inc - v;
+    *total = s_warp[32];
+    return r;
+}
+
+__global__ void scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n,
+                                   uint32_t* __restrict__ partials) {
+    __shared__ uint32_t s_warp[33];
+    int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i)
+        if (base + i < n) s += in[base + i];
+    uint32_t total;
+    block_excl_scan(s, s_warp, &total);
+    if (threadIdx.x == 0) partials[blockIdx.x] = total;
+}
+
+// Single block: exclusive scan of the per-block partials in place.
+__global__ void scan_partials_kernel(uint32_t* partials, int64_t nparts) {
+    __shared__ uint32_t s_warp[33];
+    uint32_t carry = 0;
+    for (int64_t base = 0; base < nparts; base += kScanThreads) {
+        int64_t i = base + threadIdx.x;
+        uint32_t v = i < nparts ? partials[i] : 0;
+        uint32_t total;
+        uint32_t e = block_excl_scan(v, s_warp, &total);
+        if (i < nparts) partials[i] = carry + e;
+        carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[nparts] = carry;
+}
+
+__global__ void scan_down_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                 int64_t n, const uint32_t* __restrict__ partials, int64_t nparts,
+                                 uint32_t* total_out) {
+    __shared__ uint32_t s_warp[33];
+    int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        v[i] = base + i < n ? in[base + i] : 0;
+        s += v[i];
+    }
+    uint32_t total;
+    uint32_t e = block_excl_scan(s, s_warp, &total) + partials[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        if (base + i < n) out[base + i] = e;
+        e += v[i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        out[n] = partials[nparts];
+        if (total_out) *total_out = partials[nparts];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Radix sort.  8-bit digits; each CTA owns kSortTile consecutive items and
+// processes them in rounds of 256 (one per thread) so the scatter is stable:
+// intra-warp rank from __match_any_sync, inter-warp prefix per digit in smem,
+// inter-block offsets from a digit-major exclusive scan of block histograms.
+
+constexpr int kSortThreads = 256;
+constexpr int kSortRounds = 16;
+constexpr int kSortTile = kSortThreads * kSortRounds;  // 4096
+
+__device__ __forceinline__ uint32_t sort_count(const uint32_t* n_dev, int64_t n_host, int64_t cap) {
+    int64_t n = n_dev ? (int64_t)*n_dev : n_host;
+    return (uint32_t)(n < cap ? n : cap);
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads)
+radix_upsweep_kernel(const K* __restrict__ keys, const uint32_t* n_dev, int64_t n_host, int64_t cap,
+                     int shift, uint32_t* __restrict__ hist, int nblocks) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    uint32_t n = sort_count(n_dev, n_host, cap);
+    int64_t base = (int64_t)blockIdx.x * kSortTile;
+    if (base < n) {
+        for (int r = 0; r < kSortRounds; ++r) {
+            int64_t i = base + r * kSortThreads + threadIdx.x;
+            if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 0xffu], 1u);
+        }
+    }
+    __syncthreads();
+    hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads)
+radix_downsweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                       K* __restrict__ kout, uint32_t* __restrict__ vout,
+                       const uint32_t* n_dev, int64_t n_host, int64_t cap, int shift,
+                       const uint32_t* __restrict__ hist, int nblocks) {
+    __shared__ uint32_t s_run[256];
+    __shared__ uint32_t s_wcnt[8][256];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t n = sort_count(n_dev, n_host, cap);
+    int64_t base = (int64_t)blockIdx.x * kSortTile;
+    if (base >= n) return;
+    s_run[tid] = hist[(int64_t)tid * nblocks + blockIdx.x];
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int r = 0; r < kSortRounds; ++r) {
+        int64_t i = base + r * kSortThreads + tid;
+        if (base + r * kSortThreads >= n) break;  // uniform across the block
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s_wcnt[w][tid] = 0;
+        __syncthreads();
+        bool valid = i < n;
+        K k = valid ? kin[i] : K(0);
+        uint32_t v = valid ? vin[i] : 0u;
+        uint32_t d = (uint32_t)(k >> shift) & 0xffu;
+        uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+        uint32_t rank_in_warp = 0;
+        if (valid) {
+            uint32_t peers = __match_any_sync(vmask, d);
+            rank_in_warp = __popc(peers & lt_mask);
+            if (rank_in_warp == 0) s_wcnt[warp][d] = __popc(peers);
+        }
+        __syncthreads();
+        uint32_t run = s_run[tid];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            uint32_t c = s_wcnt[w][tid];
+            s_wcnt[w][tid] = run;
+            run += c;
+        }
+        s_run[tid] = run;
+        __syncthreads();
+        if (valid) {
+            uint32_t pos = s_wcnt[warp][d] + rank_in_warp;
+            kout[pos] = k;
+            vout[pos] = v;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+int64_t scan_scratch_words(int64_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* scratch,
+                       uint32_t* total_out, cudaStream_t stream) {
+    int64_t nparts = (n + kScanTile - 1) / kScanTile;
+    if (nparts == 0) nparts = 1;
+    scan_reduce_kernel<<<(unsigned)nparts, kScanThreads, 0, stream>>>(in, n, scratch);
+    scan_partials_kernel<<<1, kScanThreads, 0, stream>>>(scratch, nparts);
+    scan_down_kernel<<<(unsigned)nparts, kScanThreads, 0, stream>>>(in, out, n, scratch, nparts,
+                                                                     total_out);
+    return SPLAT_OK;
+}
+
+int64_t radix_blocks(int64_t cap) { return (cap + kSortTile - 1) / kSortTile; }
+
+int64_t radix_scratch_words(int64_t cap) {
+    int64_t nb = radix_blocks(cap);
+    if (nb == 0) nb = 1;
+    return 256 * nb + 1 + scan_scratch_words(256 * nb + 1);
+}
+
+template <typename K>
+int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
+                     int64_t n_host, int64_t cap, int begin_bit, int end_bit, uint32_t* scratch,
+                     int* result_in_alt, cudaStream_t stream) {
+    int nb = (int)radix_blocks(cap);
+    if (nb == 0) nb = 1;
+    uint32_t* hist = scratch;
+    uint32_t* hscan = scratch + 256 * (int64_t)nb + 1;
+    K* src_k = keys;
+    uint32_t* src_v = vals;
+    K* dst_k = keys_alt;
+    uint32_t* dst_v = vals_alt;
+    int alt = 0;
+    for (int shift = begin_bit; shift < end_bit; shift += 8) {
+        radix_upsweep_kernel<K><<<nb, kSortThreads, 0, stream>>>(src_k, n_dev, n_host, cap, shift,
+                                                                 hist, nb);
+        exclusive_scan_u32(hist, hist, 256 * (int64_t)nb, hscan, nullptr, stream);
+        radix_downsweep_kernel<K><<<nb, kSortThreads, 0, stream>>>(src_k, src_v, dst_k, dst_v,
+                                                                   n_dev, n_host, cap, shift, hist, nb);
+        K* tk = src_k; src_k = dst_k; dst_k = tk;
+        uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
+        alt ^= 1;
+    }
+    *result_in_alt = alt;
+    return SPLAT_OK;
+}
+
+template int radix_sort_pairs<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, const uint32_t*,
+                                        int64_t, int64_t, int, int, uint32_t*, int*, cudaStream_t);
+template int radix_sort_pairs<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, const uint32_t*,
+                                        int64_t, int64_t, int, int, uint32_t*, int*, cudaStream_t);
+
+}  // namespace splat

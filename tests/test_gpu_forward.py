@@ -1,0 +1,156 @@
+"""GPU parity of the forward path (render + upscale) against the reference's
+golden vectors and the pinned CPU oracle.
+
+Tolerances (BASELINE.json north_star): integer work — sort order, bboxes,
+validity, tile keys / per-tile ranges, contrib_count — bit-exact; image and
+gradient planes within 1e-4 max-abs (float32 kernels vs float64 reference).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, golden_names, ref_fixture_scene, scene_of
+
+pytestmark = pytest.mark.gpu
+
+PLANE_TOL = 1e-4
+FIELDS = ("color", "d_dx", "d_dy", "d_dxdy", "alpha", "alpha_dx", "alpha_dy", "alpha_dxdy")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2503_14171_b200 as P
+    return P
+
+
+def assert_forward_matches(got, ref, name=""):
+    assert np.array_equal(got["contrib_count"], ref["contrib_count"]), \
+        (name, int((got["contrib_count"] != ref["contrib_count"]).sum()))
+    for f in FIELDS:
+        err = np.abs(got[f] - ref[f]).max() if got[f].size else 0.0
+        assert err < PLANE_TOL, (name, f, err)
+
+
+@pytest.mark.parametrize("name", golden_names("fwd_"))
+def test_forward_matches_reference_golden(P, name):
+    g = golden(name)
+    sc = scene_of(g)
+    w, h = int(g["out_w"]), int(g["out_h"])
+    img = P.render_forward(sc, w, h)
+    assert_forward_matches(img.numpy(), g, name)
+    if "up" in g:
+        up = P.upscale_spline(img, float(g["up_factor"])).cpu().numpy()
+        assert up.shape == g["up"].shape
+        assert np.abs(up - g["up"]).max() < PLANE_TOL
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("fwd_") if n != "fwd_empty"])
+def test_preprocess_and_binning_bitexact(P, name):
+    g = golden(name)
+    sc = scene_of(g)
+    w, h = int(g["out_w"]), int(g["out_h"])
+    pack = P.prepare_scene(sc, w, h)
+    assert np.array_equal(pack.order.cpu().numpy(), g["order"])
+    assert np.array_equal(pack.bboxes.cpu().numpy(), g["bboxes"])
+    assert np.array_equal(pack.valid.cpu().numpy(), g["valid"])
+    conics = pack.conics.cpu().numpy()
+    assert np.allclose(conics, g["conics"], rtol=1e-14, atol=0)
+    assert np.allclose(pack.means.cpu().numpy(), g["pmeans"], rtol=1e-15, atol=0)
+    _, bins = P.bin_tiles(pack, w, h)
+    assert np.array_equal(bins.offsets.cpu().numpy(), g["tile_off"])
+    assert np.array_equal(bins.ranks.cpu().numpy(), g["tile_ranks"])
+
+
+@pytest.mark.parametrize("name", golden_names("up_"))
+def test_upscale_matches_reference_golden(P, name):
+    g = golden(name)
+    img = P.GradientImage.from_planes(g["color"], g["d_dx"], g["d_dy"], g["d_dxdy"])
+    size = None if g["out_size"][0] < 0 else tuple(int(v) for v in g["out_size"])
+    f = float(g["factor"])
+    out = P.upscale_spline(img, f, out_size=size).cpu().numpy()
+    raw = P.upscale_spline(img, f, out_size=size, clamp=False).cpu().numpy()
+    assert out.shape == g["out"].shape
+    assert np.abs(out - g["out"]).max() < 1e-5
+    assert np.abs(raw - g["raw"]).max() < 1e-5
+    back = P.upscale_backward(img, f, g["adjoint"], out_size=size)
+    for got, key in ((back.d_color, "b_color"), (back.d_dx, "b_dx"), (back.d_dy, "b_dy"),
+                     (back.d_dxdy, "b_dxdy")):
+        ref = g[key]
+        err = np.abs(got.double().cpu().numpy() - ref).max()
+        assert err < 1e-5 * max(1.0, np.abs(ref).max()), (key, err)
+
+
+def test_upscale_factor_one_is_identity(P):
+    # reference test_spline.py:176-180: factor 1 reproduces the colour exactly
+    g = golden("up_f1")
+    img = P.GradientImage.from_planes(g["color"], g["d_dx"], g["d_dy"], g["d_dxdy"])
+    out = P.upscale_spline(img, 1.0)
+    assert np.array_equal(out.cpu().numpy(), img.color.cpu().numpy())
+
+
+def test_upscale_errors(P):
+    from paper_2503_14171_b200.core import DimensionError, UnsupportedScaleError
+    img = P.GradientImage.zeros(8, 8)
+    with pytest.raises(UnsupportedScaleError):
+        P.upscale_spline(img, 0.5)
+    with pytest.raises(DimensionError):
+        P.upscale_backward(img, 2.0, np.zeros((5, 5, 3)))
+    with pytest.raises(DimensionError):
+        P.render_forward(P.Scene.empty(), 0, 8)
+
+
+@pytest.mark.parametrize("seed,n,size", [(0, 400, 96), (1, 3000, 128), (2, 60, 64)])
+def test_forward_matches_oracle_sharp(P, oracle, seed, n, size):
+    sc = ref_fixture_scene(seed, n, size)
+    img = P.render_forward(sc, size, size - 5)
+    ref = oracle.render_forward(sc, size, size - 5)
+    assert_forward_matches(img.numpy(), {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)})
+
+
+def test_forward_matches_oracle_c2_scale(P, oracle):
+    """Config 2 (200k splats, 960x540): full-size parity incl. contrib_count."""
+    from paper_2503_14171_b200.scenes import CONFIGS, synthetic_scene
+    c = CONFIGS["c2"]
+    sc = synthetic_scene(c.n, c.width, c.height, c.scale_range, seed=5)
+    img = P.render_forward(sc, c.width, c.height)
+    ref = oracle.render_forward(sc, c.width, c.height)
+    got = img.numpy()
+    assert_forward_matches(got, {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)}, "c2")
+    up = P.upscale_spline(img, c.factor).cpu().numpy()
+    refup = oracle.upscale_spline(ref.color, ref.d_dx, ref.d_dy, ref.d_dxdy, c.factor)
+    diff = up - refup
+    assert np.abs(diff).max() < PLANE_TOL
+    psnr = 10 * np.log10(1.0 / np.mean(diff ** 2))
+    assert psnr >= 60.0
+
+
+def test_views_match_oracle(P, oracle):
+    """The view model: view v == reference render of the transformed scene."""
+    from paper_2503_14171_b200.scenes import random_views, synthetic_scene, view_scene
+    sc = synthetic_scene(20000, 240, 135, (0.5, 2.5), seed=5)
+    for v in random_views(3, 240, 135, seed=3):
+        img = P.render_forward(sc, 240, 135, view=v)
+        ref = oracle.render_forward(view_scene(sc, v), 240, 135)
+        assert_forward_matches(img.numpy(), {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)})
+
+
+def test_forward_is_deterministic(P):
+    import torch
+    sc = ref_fixture_scene(5, 2000, 128)
+    a = P.render_forward(sc, 128, 128)
+    b = P.render_forward(sc, 128, 128)
+    assert torch.equal(a.planes, b.planes) and torch.equal(a.contrib_count, b.contrib_count)
+
+
+def test_fd_gradients_match_golden(P):
+    g = golden("fd")
+    img = P.fd_gradients(g["image"])
+    for key in ("d_dx", "d_dy", "d_dxdy"):
+        assert np.abs(getattr(img, key).double().cpu().numpy() - g[key]).max() < 1e-6
+    adj = P.SourceAdjoint(__import__("torch").stack(
+        [__import__("torch").from_numpy(g[k]) for k in ("a_color", "a_dx", "a_dy", "a_dxdy")],
+        dim=2).float().cuda())
+    back = P.fd_gradients_backward(adj).double().cpu().numpy()
+    assert np.abs(back - g["back"]).max() < 1e-5
