@@ -56,8 +56,9 @@ def test_preprocess_and_binning_bitexact(P, name):
     assert np.array_equal(pack.bboxes.cpu().numpy(), g["bboxes"])
     assert np.array_equal(pack.valid.cpu().numpy(), g["valid"])
     conics = pack.conics.cpu().numpy()
-    assert np.allclose(conics, g["conics"], rtol=1e-14, atol=0)
-    assert np.allclose(pack.means.cpu().numpy(), g["pmeans"], rtol=1e-15, atol=0)
+    # device exp/cos/sin may differ from numpy by an ulp; bboxes above are still exact
+    assert np.allclose(conics, g["conics"], rtol=1e-12, atol=0)
+    assert np.array_equal(pack.means.cpu().numpy(), g["pmeans"])
     _, bins = P.bin_tiles(pack, w, h)
     assert np.array_equal(bins.offsets.cpu().numpy(), g["tile_off"])
     assert np.array_equal(bins.ranks.cpu().numpy(), g["tile_ranks"])
