@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark: upscaled 4K frames/s (x4 spline upscale) on a 1024-view batch.
+
+Workload (BASELINE.json configs[2], SURVEY.md 8(d) "C3"): synthetic 1M-splat
+scene, 960x540 render with analytic gradients, x4 gradient-aware spline
+upscale to 3840x2160, 1024 seeded camera views sharded over the ranks (one
+process per GPU, no data-path collective; strong scaling of the fixed batch).
+A step renders + upscales every view of this rank's shard.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+        torchrun --nproc-per-node N bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "upscaled frames/s (4K output, ×4) & output Mpix/s at 1/2/4/8 B200 vs CPU ref"
+WORKLOAD = ("c3: synthetic 1M-Gaussian scene, 960x540 render with analytic gradients, "
+            "x4 gradient-aware spline upscale to 3840x2160, 1024-view batch sharded over ranks")
+FP32_LANES_PER_SM = 128
+NUM_SMS = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--views", type=int, default=1024)
+    ap.add_argument("--slots", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def config_dict(args, world, views_per_rank):
+    return {"workload": WORKLOAD, "n_splats": 1_000_000, "render": [960, 540], "output": [3840, 2160],
+            "factor": 4, "views": args.views, "views_per_rank": views_per_rank,
+            "parallelism": f"view-shard x{world}",
+            "l2": "no explicit flush: each view streams ~250 MB (pack, pairs, planes, 99.5 MB output) "
+                  "through the 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port) timing
+# ---------------------------------------------------------------------------
+
+def cpu_reference_view(scene, view):
+    """One C3 view through the CPU oracle (render + x4 upscale); seconds."""
+    from oracle import oracle as O
+    from paper_2503_14171_b200.scenes import view_scene
+    t0 = time.perf_counter()
+    img = O.render_forward(view_scene(scene, view), 960, 540)
+    O.upscale_spline(img.color, img.d_dx, img.d_dy, img.d_dxdy, 4.0)
+    return time.perf_counter() - t0
+
+
+def make_workload(nviews):
+    from paper_2503_14171_b200.scenes import CONFIGS, random_views, synthetic_scene
+    c = CONFIGS["c3"]
+    scene = synthetic_scene(c.n, c.width, c.height, c.scale_range, seed=5)
+    views = random_views(nviews, c.width, c.height, seed=11)
+    return scene, views
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    scene, views = make_workload(args.views)
+    cores = O.default_threads()
+    for i in range(min(args.warmup, 1)):
+        cpu_reference_view(scene, views[i])
+    times = [cpu_reference_view(scene, views[i % len(views)]) for i in range(args.steps)]
+    per_view = sum(times) / len(times)
+    value = 1.0 / per_view
+    sample = f"1 view of the C3 batch per step (views 0..{args.steps - 1}), x1024 extrapolated"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": per_view * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, 1, args.views),
+            "mpix_per_s": value * 3840 * 2160 / 1e6,
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "note": "reference CPU path = the float64 C/numpy oracle port of splinesplat (the reference "
+                    "is a Python/numba package that cannot be shipped to the GPU box)"}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for row in open(self.path):
+            p = [x.strip() for x in row.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = max(mx, float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        busy = [s for s in sm if s > 0.5 * mx] or sm
+        busy.sort()
+        return {"sm_mhz": busy[len(busy) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import numpy as np
+    from paper_2503_14171_b200 import _lib
+    from paper_2503_14171_b200.device import DeviceScene
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+
+    lib = _lib.load()
+    scene, views = make_workload(args.views)
+    per = (len(views) + world - 1) // world
+    mine = views[rank * per:(rank + 1) * per]
+
+    pipe = ViewPipeline(scene, 960, 540, factor=4.0, slots=args.slots, views_for_capacity=mine)
+
+    # untimed: algorithmic work per view (K = sum contrib_count, E = sum valid bbox areas)
+    sample = mine[: min(16, len(mine))]
+    from paper_2503_14171_b200.raster_forward import render_forward
+    K = E = 0.0
+    for v in sample:
+        img = render_forward(pipe.scene, 960, 540, view=v)
+        K += float(img.contrib_count.sum(dtype=torch.int64))
+        bb = img.frame.bboxes().to(torch.int64)
+        area = (bb[:, 1] - bb[:, 0]) * (bb[:, 3] - bb[:, 2])
+        E += float(area[img.frame.touched() > 0].sum())
+        del img
+    K /= len(sample)
+    E /= len(sample)
+    P = 960 * 540
+    raster_flops = 27.0 * P + 13.0 * E + 69.0 * K
+    up_bytes = 12.0 * 3840 * 2160 + 48.0 * P
+
+    for _ in range(args.warmup):
+        pipe.render(mine)
+    torch.cuda.synchronize()
+    pipe.check()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.splat_kernel_launches()
+    pipe.enable_stage_timing(args.slots == 1)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(args.steps):
+        pipe.fork()
+        pipe.render(mine)
+        pipe.join()
+    end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = lib.splat_kernel_launches() - launches0
+    ms = start.elapsed_time(end) / args.steps
+    clk = clocks.stop()
+    pipe.check()
+    stage = pipe.stage_times_ms()
+    pipe.enable_stage_timing(False)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_views = per * world if world > 1 else len(mine)
+    value = total_views / (ms_max / 1e3)
+
+    # ---- e2e through the public API with host buffers -------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        host = {f: torch.from_numpy(np.ascontiguousarray(getattr(scene, f))).pin_memory()
+                for f in ("means", "log_scales", "rotations", "opacity_logits", "colors", "depths")}
+        h2d = sum(v.numel() * v.element_size() for v in host.values())
+        ring = [torch.empty((2160, 3840, 3), dtype=torch.float32).pin_memory() for _ in range(4)]
+        d2h = len(mine) * 2160 * 3840 * 3 * 4
+
+        def e2e_step():
+            dev = {k: v.to("cuda", non_blocking=True) for k, v in host.items()}
+            ds = DeviceScene(**dev, background=tuple(scene.background),
+                             reference_resolution=tuple(scene.reference_resolution)).prepare()
+            p2 = ViewPipeline(ds, 960, 540, factor=4.0, slots=args.slots, capacity=pipe.capacity)
+            p2.render(mine, host_out=ring)
+            p2.join()
+            return p2
+
+        e2e_step()
+        torch.cuda.synchronize()
+        ksteps = max(1, min(args.steps, 2))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(ksteps):
+            p2 = e2e_step()
+        s1.record()
+        torch.cuda.synchronize()
+        p2.check()
+        ems = s0.elapsed_time(s1) / ksteps
+        wall = (time.perf_counter() - t0) / ksteps * 1e3
+        et = torch.tensor([max(ems, wall)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": total_views / (float(et.item()) / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps": ksteps, "api": "DeviceScene upload + prepare, ViewPipeline.render(host_out=pinned ring)"}
+
+    # ---- roofline ------------------------------------------------------------------------------
+    sm_mhz = (clk or {}).get("sm_mhz") or 1335.0
+    fp32_peak = NUM_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm_peak, hbm_src = float(peaks["hbm_gbs"]), "measured"
+    except Exception:
+        hbm_peak, hbm_src = 6650.0, "fallback"
+    traffic = {}
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        pass
+    roof = None
+    roof_up = None
+    if stage:
+        r_ms = stage["raster"]
+        roof = {"kernel": "raster_fwd_kernel + fixup_kernel (per view)", "bound": "fp32",
+                "achieved": raster_flops / (r_ms * 1e-3) / 1e12,
+                "peak": fp32_peak, "unit": "TFLOP/s", "frac": raster_flops / (r_ms * 1e-3) / 1e12 / fp32_peak,
+                "traffic": traffic.get("raster_fwd_kernel"),
+                "algorithmic": {"flops_per_view": raster_flops, "K_contrib_per_view": K,
+                                "E_bbox_evals_per_view": E, "formula": "27P + 13E + 69K (SURVEY 8d)"},
+                "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (median SM clock in run)"}
+        u_ms = stage["upscale"]
+        roof_up = {"kernel": "upscale_fwd_kernel", "bound": "hbm",
+                   "achieved": up_bytes / (u_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                   "frac": up_bytes / (u_ms * 1e-3) / 1e9 / hbm_peak,
+                   "traffic": traffic.get("upscale_fwd_kernel"),
+                   "algorithmic_bytes": up_bytes, "peak_source": hbm_src}
+
+    # ---- CPU baseline (rank 0, N=1 only) ---------------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        O.build()
+        tcpu = cpu_reference_view(scene, mine[0])
+        cpu = {"value": 1.0 / tcpu, "unit": "frames/s", "cores": O.default_threads(), "kind": "port",
+               "sample": "1 view of the C3 batch through the float64 oracle (render + x4 upscale)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": config_dict(args, world, len(mine)),
+                "mpix_per_s": value * 3840 * 2160 / 1e6,
+                "stage_ms_per_view": stage, "gpu_launches": int(launches),
+                "roofline": roof, "roofline_upscale": roof_up, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

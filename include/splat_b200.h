@@ -77,13 +77,16 @@ typedef struct {
     uint32_t *keys;         /* (capacity) sorted tile id per pair */
     uint32_t *ranks;        /* (capacity) sorted rank per pair */
     uint32_t *ranges;       /* (ntiles,2) [start,end) into keys/ranks */
-    uint32_t *counters;     /* [0]=pairs [1]=overflow [2]=fix-up pixels [3]=fix-up capacity hit */
+    uint32_t *counters;     /* [0]=pairs [1]=overflow [2]=fix-up pixels; [4]=sticky overflow
+                               (never cleared by the library: the caller zeroes it) */
     uint32_t *fixup;        /* (H*W) pixels re-rendered by the exact float64 pass */
     float *pack;            /* (n,12) float32 per-view pack */
 } splat_frame_ptrs_t;
 
 const char *splat_last_error(void);
 int splat_abi_version(void);
+/* Number of kernels this library has launched since load (all streams). */
+uint64_t splat_kernel_launches(void);
 
 /* ---- per-scene preparation (view independent) --------------------------
  * Stable depth argsort (raster_forward.py:59-61) and the view-independent
@@ -114,6 +117,11 @@ int splat_prepare_view(const void *scene_const, int64_t n, const splat_view_t *v
                        int height, void *workspace, size_t ws_bytes, int64_t pair_capacity,
                        void *stream);
 int splat_bin_tiles(int64_t n, int width, int height, void *workspace, size_t ws_bytes,
+                    int64_t pair_capacity, void *stream);
+/* Rasterizer + exact fix-up pass alone, on a frame already prepared and binned
+ * by the two calls above (render_forward = prepare_view + bin_tiles + rasterize). */
+int splat_rasterize(const void *scene_const, int64_t n, const splat_view_t *view, int width,
+                    int height, int train, const splat_gimg_t *out, void *workspace, size_t ws_bytes,
                     int64_t pair_capacity, void *stream);
 /* Exact float64 RenderPack of a view (prepare_scene means/conics/sigmas,
  * raster_forward.py:86-102), rank order: pack64 (n,6) = mx,my,a,b,c,sigma;

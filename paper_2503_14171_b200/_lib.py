@@ -50,6 +50,7 @@ class FramePtrsT(ctypes.Structure):
 SIGNATURES = {
     "splat_last_error": (ctypes.c_char_p, []),
     "splat_abi_version": (I32, []),
+    "splat_kernel_launches": (ctypes.c_uint64, []),
     "splat_scene_const_bytes": (SZ, [I64]),
     "splat_scene_workspace_bytes": (SZ, [I64]),
     "splat_scene_prepare": (I32, [ctypes.POINTER(SceneT), P, SZ, P, SZ, P]),
@@ -60,6 +61,8 @@ SIGNATURES = {
                                    ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_prepare_view": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, P, SZ, I64, P]),
     "splat_bin_tiles": (I32, [I64, I32, I32, P, SZ, I64, P]),
+    "splat_rasterize": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
+                              ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_view_pack64": (I32, [P, I64, ctypes.POINTER(ViewT), P, P]),
     "splat_upscale_forward": (I32, [P, I32, I32, P, I32, I32, I32, P]),
     "splat_upscale_backward": (I32, [P, I32, I32, P, I32, I32, P]),

@@ -1,5 +1,6 @@
 // extern "C" boundary of libsplat_b200.so (declared in include/splat_b200.h).
 #include <cstdio>
+#include <atomic>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -7,6 +8,9 @@
 namespace splat {
 
 static thread_local char g_err[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int set_error(int code, const char* msg) {
     std::snprintf(g_err, sizeof(g_err), "%s", msg);
@@ -45,6 +49,7 @@ extern "C" {
 
 const char* splat_last_error(void) { return g_err; }
 int splat_abi_version(void) { return SPLAT_ABI_VERSION; }
+uint64_t splat_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 size_t splat_scene_const_bytes(int64_t n) { return const_layout(n).total; }
 size_t splat_scene_workspace_bytes(int64_t n) { return scene_workspace_bytes_impl(n); }
@@ -123,6 +128,18 @@ int splat_render_forward(const void* scene_const, int64_t n, const splat_view_t*
     if ((rc = launch_preprocess(sc, vc, L, w, s))) return rc;
     if ((rc = launch_binning(L, w, s))) return rc;
     return launch_raster_forward(sc, vc, L, w, *out, train != 0, s);
+}
+
+int splat_rasterize(const void* scene_const, int64_t n, const splat_view_t* view, int width, int height,
+                    int train, const splat_gimg_t* out, void* workspace, size_t ws_bytes,
+                    int64_t pair_capacity, void* stream) {
+    int rc = check_dims(width, height);
+    if (rc) return rc;
+    if (train && !out->state) return set_error(SPLAT_ERR_PARAMETER, "train mode needs the state buffer");
+    FrameLayout L = frame_layout(n, width, height, pair_capacity);
+    if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    return launch_raster_forward(scene_const_view(scene_const, n), make_view_const(*view), L,
+                                 (char*)workspace, *out, train != 0, (cudaStream_t)stream);
 }
 
 int splat_upscale_forward(const float* src, int in_w, int in_h, float* out, int out_w, int out_h, int clamp,

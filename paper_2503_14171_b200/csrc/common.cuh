@@ -48,6 +48,7 @@ __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; 
     } while (0)
 
 namespace splat {
+void note_launch();  // counts kernels launched by this library (splat_kernel_launches)
 int set_cuda_error(cudaError_t e, const char* what);
 int set_error(int code, const char* msg);
 }  // namespace splat

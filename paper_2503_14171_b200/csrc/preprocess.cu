@@ -132,6 +132,7 @@ __global__ void emit_pairs_kernel(int64_t n, const short4* __restrict__ bboxes,
     uint32_t off = offsets[r];
     if ((int64_t)off + cnt > cap) {
         atomicOr(&counters[1], 1u);
+        atomicOr(&counters[4], 1u);  // sticky until the caller clears it
         return;
     }
     short4 bb = bboxes[r];
@@ -273,7 +274,7 @@ int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaSt
     uint32_t* v1 = (uint32_t*)(w + 2 * align_up(nn * 8) + align_up(nn * 4));
     uint32_t* scratch = (uint32_t*)(w + 2 * align_up(nn * 8) + 2 * align_up(nn * 4));
     int blocks = (int)((n + 255) / 256);
-    depth_keys_kernel<<<blocks, 256, 0, stream>>>(s.depths, n, k0, v0);
+    depth_keys_kernel<<<blocks, 256, 0, stream>>>(s.depths, n, k0, v0); note_launch();
     int alt = 0;
     radix_sort_pairs<uint64_t>(k0, v0, k1, v1, nullptr, n, n, 0, 64, scratch, &alt, stream);
     const uint32_t* order = alt ? v1 : v0;
@@ -283,7 +284,7 @@ int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaSt
         n, order, s.means, s.log_scales, s.rotations, s.opacity_logits, s.colors,
         (int32_t*)(b + L.order), (double*)(b + L.mean), (double*)(b + L.n00), (double*)(b + L.n01),
         (double*)(b + L.n11), (double*)(b + L.e1e2), (double*)(b + L.sigma), (double*)(b + L.q),
-        (float4*)(b + L.color));
+        (float4*)(b + L.color)); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
@@ -291,12 +292,12 @@ int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaSt
 int launch_preprocess(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
                       cudaStream_t stream) {
     uint32_t* counters = (uint32_t*)(ws + L.counters);
-    SPLAT_CUDA_CHECK(cudaMemsetAsync(counters, 0, 16 * 4, stream));
+    SPLAT_CUDA_CHECK(cudaMemsetAsync(counters, 0, 4 * 4, stream));  // [4..] are sticky
     if (sc.n == 0) return SPLAT_OK;
     int blocks = (int)((sc.n + 255) / 256);
     preprocess_kernel<<<blocks, 256, 0, stream>>>(sc, vc, L.width, L.height,
                                                   (PackF*)(ws + L.pack), (short4*)(ws + L.bboxes),
-                                                  (uint32_t*)(ws + L.touched));
+                                                  (uint32_t*)(ws + L.touched)); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
@@ -316,21 +317,21 @@ int launch_binning(const FrameLayout& L, char* ws, cudaStream_t stream) {
     uint32_t* k1 = (uint32_t*)(ws + L.keys1);
     uint32_t* v1 = (uint32_t*)(ws + L.vals1);
     emit_pairs_kernel<<<blocks, 256, 0, stream>>>(L.n, (const short4*)(ws + L.bboxes), touched,
-                                                  offsets, L.ntx, L.cap, k0, v0, counters);
+                                                  offsets, L.ntx, L.cap, k0, v0, counters); note_launch();
     int alt = 0;
     radix_sort_pairs<uint32_t>(k0, v0, k1, v1, counters, 0, L.cap, 0, tile_key_bits(ntiles),
                                (uint32_t*)(ws + L.sort_scratch), &alt, stream);
     const uint32_t* keys = alt ? k1 : k0;
     int rblocks = (int)((L.cap + 255) / 256);
     if (rblocks > 0)
-        tile_ranges_kernel<<<rblocks, 256, 0, stream>>>(keys, counters, L.cap, ranges);
+        tile_ranges_kernel<<<rblocks, 256, 0, stream>>>(keys, counters, L.cap, ranges); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
 
 int launch_pack64(const SceneConst& sc, const ViewConst& vc, double* out, cudaStream_t stream) {
     if (sc.n == 0) return SPLAT_OK;
-    pack64_kernel<<<(int)((sc.n + 255) / 256), 256, 0, stream>>>(sc, vc, out);
+    pack64_kernel<<<(int)((sc.n + 255) / 256), 256, 0, stream>>>(sc, vc, out); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }

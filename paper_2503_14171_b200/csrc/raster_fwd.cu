@@ -443,11 +443,11 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
     a.counters = (uint32_t*)(ws + L.counters);
     int ntiles = L.ntx * L.nty;
     if (train) {
-        raster_fwd_kernel<true><<<ntiles, kBlock, 0, stream>>>(a);
-        fixup_kernel<true><<<148 * 2, 256, 0, stream>>>(a);
+        raster_fwd_kernel<true><<<ntiles, kBlock, 0, stream>>>(a); note_launch();
+        fixup_kernel<true><<<148 * 2, 256, 0, stream>>>(a); note_launch();
     } else {
-        raster_fwd_kernel<false><<<ntiles, kBlock, 0, stream>>>(a);
-        fixup_kernel<false><<<148 * 2, 256, 0, stream>>>(a);
+        raster_fwd_kernel<false><<<ntiles, kBlock, 0, stream>>>(a); note_launch();
+        fixup_kernel<false><<<148 * 2, 256, 0, stream>>>(a); note_launch();
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;

@@ -186,10 +186,10 @@ int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* s
                        uint32_t* total_out, cudaStream_t stream) {
     int64_t nparts = (n + kScanTile - 1) / kScanTile;
     if (nparts == 0) nparts = 1;
-    scan_reduce_kernel<<<(unsigned)nparts, kScanThreads, 0, stream>>>(in, n, scratch);
-    scan_partials_kernel<<<1, kScanThreads, 0, stream>>>(scratch, nparts);
+    scan_reduce_kernel<<<(unsigned)nparts, kScanThreads, 0, stream>>>(in, n, scratch); note_launch();
+    scan_partials_kernel<<<1, kScanThreads, 0, stream>>>(scratch, nparts); note_launch();
     scan_down_kernel<<<(unsigned)nparts, kScanThreads, 0, stream>>>(in, out, n, scratch, nparts,
-                                                                     total_out);
+                                                                     total_out); note_launch();
     return SPLAT_OK;
 }
 
@@ -216,10 +216,10 @@ int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, c
     int alt = 0;
     for (int shift = begin_bit; shift < end_bit; shift += 8) {
         radix_upsweep_kernel<K><<<nb, kSortThreads, 0, stream>>>(src_k, n_dev, n_host, cap, shift,
-                                                                 hist, nb);
+                                                                 hist, nb); note_launch();
         exclusive_scan_u32(hist, hist, 256 * (int64_t)nb, hscan, nullptr, stream);
         radix_downsweep_kernel<K><<<nb, kSortThreads, 0, stream>>>(src_k, src_v, dst_k, dst_v,
-                                                                   n_dev, n_host, cap, shift, hist, nb);
+                                                                   n_dev, n_host, cap, shift, hist, nb); note_launch();
         K* tk = src_k; src_k = dst_k; dst_k = tk;
         uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
         alt ^= 1;

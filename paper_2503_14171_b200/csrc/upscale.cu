@@ -381,7 +381,7 @@ int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int o
     if (smem > 200 * 1024) return set_error(SPLAT_ERR_DIMENSION, "upscale tile exceeds shared memory");
     dim3 grid(ceil_div(out_w, kUpCols), ceil_div(out_h, kUpRows));
     upscale_fwd_kernel<<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h, sx, sy, clamp,
-                                                    span_cols, span_rows);
+                                                    span_cols, span_rows); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
@@ -401,22 +401,22 @@ int upscale_backward_impl(const float* adj, int out_w, int out_h, float* dsrc, i
     if (smem > 200 * 1024) return set_error(SPLAT_ERR_DIMENSION, "upscale backward tile too large");
     dim3 grid(ceil_div(in_w, kBwCols), ceil_div(in_h, kBwRows));
     upscale_bwd_kernel<<<grid, 256, smem, stream>>>(adj, out_w, out_h, dsrc, in_w, in_h, sx, sy, max_u,
-                                                    max_v);
+                                                    max_v); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
 
 int fd_forward_impl(const float* img, int w, int h, float* planes, cudaStream_t stream) {
     dim3 grid(ceil_div(w, 128), h);
-    fd_kernel<<<grid, 128, 0, stream>>>(img, w, h, planes);
+    fd_kernel<<<grid, 128, 0, stream>>>(img, w, h, planes); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
 
 int fd_backward_impl(const float* dplanes, int w, int h, float* tmp, float* out, cudaStream_t stream) {
     dim3 grid(ceil_div(w, 128), h);
-    fd_bwd_x_kernel<<<grid, 128, 0, stream>>>(dplanes, w, h, tmp);
-    fd_bwd_kernel<<<grid, 128, 0, stream>>>(dplanes, tmp, w, h, out);
+    fd_bwd_x_kernel<<<grid, 128, 0, stream>>>(dplanes, w, h, tmp); note_launch();
+    fd_bwd_kernel<<<grid, 128, 0, stream>>>(dplanes, tmp, w, h, out); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }

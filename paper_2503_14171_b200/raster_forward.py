@@ -143,6 +143,7 @@ class Frame:
         self.ptrs = _lib.FramePtrsT()
         _lib.check(lib.splat_frame_pointers(_lib.ptr(self.ws), n, width, height, self.capacity,
                                             self.ptrs))
+        self.counters().zero_()
 
     def _view(self, ptr, count, dtype, shape):
         off = ptr - self.ws.data_ptr()
