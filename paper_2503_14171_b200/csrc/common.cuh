@@ -34,7 +34,7 @@ struct SceneConst {
 struct __align__(16) PackF {
     float mxh, mxl, myh, myl;     // render-space mean as float hi + lo parts
     float a, b, c, sigma;         // conic and opacity
-    float qcull, qclamp, pad0, pad1;  // ln(255 sigma), ln(sigma / 0.999)
+    float qcull, qclamp, pad0, pad1;  // ln(255 sigma), ln(sigma / 0.999), b/a, b/c
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

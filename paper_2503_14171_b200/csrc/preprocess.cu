@@ -115,8 +115,8 @@ __global__ void preprocess_kernel(SceneConst sc, ViewConst vc, int width, int he
     p.sigma = (float)sg;
     p.qcull = (float)q;
     p.qclamp = (float)log(sg / kAlphaClamp);
-    p.pad0 = 0.f;
-    p.pad1 = 0.f;
+    p.pad0 = (float)(b / a);  // ellipse-rectangle test: edge minimisers (raster_fwd.cu)
+    p.pad1 = (float)(b / c);
     pack[r] = p;
 }
 
@@ -133,13 +133,15 @@ __global__ void emit_pairs_kernel(int64_t n, const short4* __restrict__ bboxes,
     if ((int64_t)off + cnt > cap) {
         atomicOr(&counters[1], 1u);
         atomicOr(&counters[4], 1u);  // sticky until the caller clears it
-        return;
     }
+    // pairs beyond the capacity are dropped (and flagged above); every slot
+    // below min(total, cap) is still written so later stages never read garbage
     short4 bb = bboxes[r];
     int tx0 = bb.x / kTile, tx1 = (bb.y - 1) / kTile;
     int ty0 = bb.z / kTile, ty1 = (bb.w - 1) / kTile;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
+            if ((int64_t)off >= cap) return;
             keys[off] = (uint32_t)(ty * ntx + tx);
             ranks[off] = (uint32_t)r;
             ++off;
@@ -147,12 +149,13 @@ __global__ void emit_pairs_kernel(int64_t n, const short4* __restrict__ bboxes,
 }
 
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const uint32_t* counters,
-                                   int64_t cap, uint32_t* __restrict__ ranges) {
+                                   int64_t cap, int ntiles, uint32_t* __restrict__ ranges) {
     int64_t np = counters[0];
     if (np > cap) np = cap;
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= np) return;
     uint32_t k = keys[j];
+    if (k >= (uint32_t)ntiles) return;  // defensive: never index past the range table
     if (j == 0 || keys[j - 1] != k) ranges[2 * k] = (uint32_t)j;
     if (j == np - 1 || keys[j + 1] != k) ranges[2 * k + 1] = (uint32_t)(j + 1);
 }
@@ -324,7 +327,7 @@ int launch_binning(const FrameLayout& L, char* ws, cudaStream_t stream) {
     const uint32_t* keys = alt ? k1 : k0;
     int rblocks = (int)((L.cap + 255) / 256);
     if (rblocks > 0)
-        tile_ranges_kernel<<<rblocks, 256, 0, stream>>>(keys, counters, L.cap, ranges); note_launch();
+        tile_ranges_kernel<<<rblocks, 256, 0, stream>>>(keys, counters, L.cap, ntiles, ranges); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }

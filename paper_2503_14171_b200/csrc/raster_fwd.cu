@@ -208,19 +208,31 @@ struct Blend {
     }
 };
 
-__device__ __forceinline__ uint8_t warp_mask_of(short4 bb, int tx0, int ty0) {
-    // bit (row*2 + col): warp rectangle col in {0,1} (8 px), row in {0..3} (4 px)
-    uint32_t cols = 0, rows = 0;
-    if (bb.x < tx0 + 8 && bb.y > tx0) cols |= 1u;
-    if (bb.x < tx0 + 16 && bb.y > tx0 + 8) cols |= 2u;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-        if (bb.z < ty0 + 4 * (r + 1) && bb.w > ty0 + 4 * r) rows |= 1u << r;
-    uint32_t m = 0;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-        if (rows & (1u << r)) m |= cols << (2 * r);
-    return (uint8_t)m;
+// Conservative "does the cull ellipse {Q <= qcull} reach the pixel-centre
+// rectangle [X0,X1] x [Y0,Y1]" test.  The minimum of the positive-definite
+// form over the rectangle is at the centre (if inside) or on an edge, where it
+// is a 1-D quadratic minimised in closed form.  Each edge value is lowered by
+// a bound on its float32 error (2^-18 (a u^2 + c v^2) >= 8 ulp * s) before the
+// comparison, and NaNs keep the candidate, so no contributing candidate is
+// ever rejected.  pad0/pad1 of the pack hold b/a and b/c.
+__device__ __forceinline__ bool ellipse_hits_rect(const PackF& g, float X0, float X1, float Y0, float Y1) {
+    const float u0 = (X0 - g.mxh) - g.mxl, u1 = (X1 - g.mxh) - g.mxl;
+    const float v0 = (Y0 - g.myh) - g.myl, v1 = (Y1 - g.myh) - g.myl;
+    if (u0 <= 0.f && u1 >= 0.f && v0 <= 0.f && v1 >= 0.f) return true;
+    const float b2 = 2.f * g.b;
+    float lo = 3.0e38f;
+    auto edge = [&](float u, float v) {
+        float t1 = (g.a * u) * u, t3 = (g.c * v) * v;
+        float qv = fmaf(b2 * u, v, t1 + t3);
+        lo = fminf(lo, fmaf(-(t1 + t3), 3.8146973e-06f, qv));
+    };
+    // vertical edges u = u0, u1: v* = -(b/c) u clamped
+    edge(u0, fminf(fmaxf(-g.pad1 * u0, v0), v1));
+    edge(u1, fminf(fmaxf(-g.pad1 * u1, v0), v1));
+    // horizontal edges v = v0, v1: u* = -(b/a) v clamped
+    edge(fminf(fmaxf(-g.pad0 * v0, u0), u1), v0);
+    edge(fminf(fmaxf(-g.pad0 * v1, u0), u1), v1);
+    return !(lo > fmaf(g.qcull, 3.8146973e-06f, g.qcull));
 }
 
 template <bool TRAIN>
@@ -264,23 +276,61 @@ __device__ __forceinline__ void write_pixel(const RasterArgs& p, int px, int py,
 }
 
 constexpr float kTermF = 1e-4f;
+constexpr int kWarps = kBlock / 32;
 
+// One candidate at one pixel: certified decision, blend, termination test.
 template <bool TRAIN>
-__global__ void __launch_bounds__(kBlock) raster_fwd_kernel(RasterArgs p) {
-    __shared__ PackF s_pack[kBlock];
-    __shared__ float4 s_col[kBlock];
-    __shared__ uint32_t s_rank[kBlock];
-    __shared__ uint8_t s_mask[kBlock];
+__device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF& g, const float4& col,
+                                                uint32_t r, uint32_t j, int px, int py, float cx,
+                                                float cy, Blend<TRAIN>& s, bool& active, bool& flagged) {
+    float al, gax, gay, gaxy, rel;
+    int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
+    if (st == kCulled) return;
+    if (st == kUnsure) {
+        double a64;
+        st = eval_exact(p.sc, p.vc, p.bboxes, r, px, py, &a64);
+        if (st == kCulled) return;
+        canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
+    }
+    float om = 1.f - al;
+    if (st == kClamped) {
+        om = 1.0e-3f;
+        rel = 0.f;
+    }
+    s.add(al, gax, gay, gaxy, om, col);
+    s.last = j + 1;
+    // relative error bound of T: error of om plus one rounding of the product
+    s.eps += fmaf(__fdividef(al, om), rel, 1.2e-7f);
+    const float m = fmaf(4.f, s.eps, 2e-6f);
+    const float T = s.T;
+    if (T < kTermF * (1.f - m)) {
+        active = false;  // certainly terminated (_kernels.py:110-111)
+    } else if (T <= kTermF * (1.f + m)) {
+        active = false;  // too close to call in float32: exact re-render
+        flagged = true;
+    }
+}
+
+// Each warp streams the tile's candidate list itself (no block barriers):
+// 32 candidates per step are loaded one per lane, culled against the warp's
+// 8x4 pixel rectangle with the exact ellipse test, compacted into the warp's
+// shared-memory slice, then blended in depth order by every lane (pixel).
+template <bool TRAIN>
+__global__ void __launch_bounds__(kBlock, 3) raster_fwd_kernel(RasterArgs p) {
+    __shared__ PackF s_pack[kWarps][32];
+    __shared__ float4 s_col[kWarps][32];
+    __shared__ uint2 s_id[kWarps][32];   // (rank, list index)
 
     const int tile = blockIdx.x;
     const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int tx0 = tile_x * kTile, ty0 = tile_y * kTile;
-    const int px = tx0 + (warp & 1) * 8 + (lane & 7);
-    const int py = ty0 + (warp >> 1) * 4 + (lane >> 3);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rx0 = tile_x * kTile + (warp & 1) * 8, ry0 = tile_y * kTile + (warp >> 1) * 4;
+    const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3);
     const bool inside = px < p.width && py < p.height;
     const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
+    const float X0 = (float)rx0 + 0.5f, X1 = X0 + 7.f, Y0 = (float)ry0 + 0.5f, Y1 = Y0 + 3.f;
     const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
+    const uint32_t lt = (1u << lane) - 1u;
 
     Blend<TRAIN> s;
     s.init();
@@ -288,57 +338,36 @@ __global__ void __launch_bounds__(kBlock) raster_fwd_kernel(RasterArgs p) {
     bool active = inside;
     bool flagged = false;
 
-    for (uint32_t base = start; base < end; base += kBlock) {
-        if (__syncthreads_count(active) == 0) break;
-        uint32_t j = base + tid;
-        uint8_t m = 0;
-        if (j < end) {
-            uint32_t r = p.ranks[j];
-            short4 bb = p.bboxes[r];
-            m = warp_mask_of(bb, tx0, ty0);
-            s_pack[tid] = p.pack[r];
-            s_col[tid] = p.sc.color[r];
-            s_rank[tid] = r;
-        }
-        s_mask[tid] = m;
-        __syncthreads();
-        const int nb = (int)min((uint32_t)kBlock, end - base);
-        if (__any_sync(0xffffffffu, active)) {
-            for (int chunk = 0; chunk < nb; chunk += 32) {
-                uint32_t bits = __ballot_sync(0xffffffffu, (s_mask[chunk + lane] >> warp) & 1u);
-                while (bits) {
-                    const int k = chunk + __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    if (active) {
-                        const PackF g = s_pack[k];
-                        float al, gax, gay, gaxy, rel = 0.f;
-                        int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
-                        if (st == kUnsure) {
-                            double a64;
-                            st = eval_exact(p.sc, p.vc, p.bboxes, s_rank[k], px, py, &a64);
-                            if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
-                        }
-                        if (st != kCulled) {
-                            float om = st == kClamped ? 1.0e-3f : 1.f - al;
-                            if (st == kClamped) rel = 0.f;
-                            s.add(al, gax, gay, gaxy, om, s_col[k]);
-                            s.last = base + k + 1;
-                            // relative error of om, plus one rounding of the product
-                            s.eps += fmaf(__fdividef(al, om), rel, 1.2e-7f);
-                            float T = s.T;
-                            float m_ = fmaf(4.f, s.eps, 2e-6f);
-                            if (T < kTermF * (1.f - m_)) {
-                                active = false;  // certainly terminated (_kernels.py:110-111)
-                            } else if (T <= kTermF * (1.f + m_)) {
-                                active = false;  // too close to call: exact re-render
-                                flagged = true;
-                            }
-                        }
-                    }
-                    if (!__any_sync(0xffffffffu, active)) break;
-                }
-                if (!__any_sync(0xffffffffu, active)) break;
+    if (__any_sync(0xffffffffu, active)) {
+        for (uint32_t base = start; base < end; base += 32) {
+            const uint32_t j = base + lane;
+            bool keep = false;
+            PackF g;
+            uint32_t r = 0;
+            if (j < end) {
+                r = p.ranks[j];
+                g = p.pack[r];
+                keep = ellipse_hits_rect(g, X0, X1, Y0, Y1);
             }
+            const uint32_t m = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int pos = __popc(m & lt);
+                s_pack[warp][pos] = g;
+                s_col[warp][pos] = p.sc.color[r];
+                s_id[warp][pos] = make_uint2(r, j);
+            }
+            __syncwarp();
+            const int cnt = __popc(m);
+            for (int k = 0; k < cnt; ++k) {
+                if (active) {
+                    const uint2 id = s_id[warp][k];
+                    blend_candidate<TRAIN>(p, s_pack[warp][k], s_col[warp][k], id.x, id.y, px, py, cx, cy,
+                                           s, active, flagged);
+                }
+                if ((k & 7) == 7 && !__any_sync(0xffffffffu, active)) break;
+            }
+            if (!__any_sync(0xffffffffu, active)) break;
+            __syncwarp();
         }
     }
     if (inside) {
@@ -350,11 +379,12 @@ __global__ void __launch_bounds__(kBlock) raster_fwd_kernel(RasterArgs p) {
     }
 }
 
-// Exact re-render of flagged pixels: one warp per pixel.  Lanes evaluate 32
-// candidates at a time with the exact float64 test, then the warp walks the
-// contributors in order, running the reference's float64 accumulation
-// `acc = acc + alpha * (1 - acc)` for the termination decision and the usual
-// float32 (or TRAIN float64) value recurrences for the outputs.
+// Exact re-render of flagged pixels: one warp per pixel.  Lanes screen 32
+// candidates at a time with the certified float32 test and run the exact
+// float64 reference test only where it cannot decide; the warp then walks the
+// contributors in order with the reference's float64 accumulation
+// `acc = acc + alpha * (1 - acc)` deciding termination (_kernels.py:105-111),
+// and the same float32 (or TRAIN float64) value recurrences as the main pass.
 template <bool TRAIN>
 __global__ void __launch_bounds__(256) fixup_kernel(RasterArgs p) {
     const int lane = threadIdx.x & 31;
@@ -372,20 +402,21 @@ __global__ void __launch_bounds__(256) fixup_kernel(RasterArgs p) {
         double acc = 0.0;
         bool done = false;
         for (uint32_t base = start; base < end && !done; base += 32) {
-            uint32_t j = base + lane;
+            const uint32_t j = base + lane;
             int st = kCulled;
             double a64 = 0.0;
-            uint32_t r = 0;
-            if (j < end) {
-                r = p.ranks[j];
-                st = eval_exact(p.sc, p.vc, p.bboxes, r, px, py, &a64);
-            }
-            float al = 0.f, gax = 0.f, gay = 0.f, gaxy = 0.f;
+            float al = 0.f, gax = 0.f, gay = 0.f, gaxy = 0.f, rel;
             float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (st != kCulled) {
+            if (j < end) {
+                const uint32_t r = p.ranks[j];
                 const PackF g = p.pack[r];
-                canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
-                col = p.sc.color[r];
+                st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
+                if (st != kCulled) {
+                    // the exact alpha drives the termination chain
+                    st = eval_exact(p.sc, p.vc, p.bboxes, r, px, py, &a64);
+                    if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
+                    col = p.sc.color[r];
+                }
             }
             uint32_t bits = __ballot_sync(0xffffffffu, st != kCulled);
             while (bits) {
@@ -405,8 +436,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(RasterArgs p) {
                 const float om = stk == kClamped ? 1.0e-3f : 1.f - alk;
                 s.add(alk, axk, ayk, axyk, om, ck);
                 s.last = base + k + 1;
-                // reference accumulation and test (_kernels.py:105-111)
-                double t = __dsub_rn(1.0, acc);
+                const double t = __dsub_rn(1.0, acc);
                 acc = __dadd_rn(acc, __dmul_rn(ak, t));
                 if (__dsub_rn(1.0, acc) < kEarlyTerm) {
                     done = true;

@@ -1,0 +1,51 @@
+"""The batched multi-view pipeline equals per-view render_forward + upscale_spline."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_pipeline_matches_single_view_api():
+    import torch
+    import paper_2503_14171_b200 as P
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    sc = P.synthetic_scene(30000, 320, 180, (0.5, 2.5), seed=5)
+    views = P.random_views(5, 320, 180, seed=2)
+    for slots in (1, 3):
+        pipe = ViewPipeline(sc, 320, 180, factor=4.0, slots=slots, views_for_capacity=views)
+        outs = pipe.render(views, keep=True)
+        pipe.join()
+        torch.cuda.synchronize()
+        pipe.check()
+        for v, got in zip(views, outs):
+            ref = P.upscale_spline(P.render_forward(sc, 320, 180, view=v), 4.0)
+            assert torch.equal(got, ref)
+
+
+def test_pipeline_host_ring_copies():
+    import torch
+    import paper_2503_14171_b200 as P
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    sc = P.synthetic_scene(5000, 96, 54, (0.5, 2.5), seed=1)
+    views = P.random_views(4, 96, 54, seed=3)
+    pipe = ViewPipeline(sc, 96, 54, factor=2.0, slots=2, views_for_capacity=views)
+    ring = [torch.empty((108, 192, 3)).pin_memory() for _ in range(4)]
+    pipe.render(views, host_out=ring)
+    pipe.join()
+    torch.cuda.synchronize()
+    for i, v in enumerate(views):
+        ref = P.upscale_spline(P.render_forward(sc, 96, 54, view=v), 2.0).cpu()
+        assert torch.equal(ring[i], ref)
+
+
+def test_pipeline_overflow_is_detected():
+    import torch
+    import paper_2503_14171_b200 as P
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    sc = P.synthetic_scene(5000, 96, 54, (0.5, 2.5), seed=1)
+    pipe = ViewPipeline(sc, 96, 54, factor=2.0, capacity=100)
+    pipe.render([None])
+    torch.cuda.synchronize()
+    with pytest.raises(RuntimeError):
+        pipe.check()
