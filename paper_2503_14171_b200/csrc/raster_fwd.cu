@@ -45,8 +45,9 @@ struct RasterArgs {
 
 // Exact reference evaluation of one candidate at one pixel centre
 // (_kernels.py:61-80, float64, every operation individually rounded).
-__device__ __noinline__ int eval_exact(const SceneConst& sc, const ViewConst& vc, const short4* bboxes,
-                                       uint32_t r, int px, int py, double* alpha64) {
+__device__ __forceinline__ int eval_exact_inl(const SceneConst& sc, const ViewConst& vc,
+                                              const short4* bboxes, uint32_t r, int px, int py,
+                                              double* alpha64) {
     short4 bb = bboxes[r];
     if (px < bb.x || px >= bb.y || py < bb.z || py >= bb.w) return kCulled;
     double mx = __dmul_rn(__dsub_rn(sc.mean[2 * r], vc.ox), vc.kx);
@@ -71,6 +72,13 @@ __device__ __noinline__ int eval_exact(const SceneConst& sc, const ViewConst& vc
     return kContrib;
 }
 
+// Out-of-line copy for the main pass, where the exact path is rare and must
+// not inflate the register footprint of the hot loop.
+__device__ __noinline__ int eval_exact(const SceneConst& sc, const ViewConst& vc, const short4* bboxes,
+                                       uint32_t r, int px, int py, double* alpha64) {
+    return eval_exact_inl(sc, vc, bboxes, r, px, py, alpha64);
+}
+
 // Float32 footprint with a certified decision (_kernels.py:65-87).  Returns
 // kCulled / kContrib / kClamped when the float32 evaluation decides the
 // reference's tests with margin, kUnsure otherwise.  `al` etc. are the
@@ -89,7 +97,8 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
     float s = (t1 + fabsf(t2)) + t3;
     // |qf - Q_exact| <= ~8 ulp * s; conic/mean rounding adds ~4 ulp * s.  2^-19 * s is a 2x margin.
     float tol = fmaf(s + g.qcull, 1.9073486e-06f, 1e-30f);
-    rel = fmaf(s, 4.7683716e-07f, 1.9073486e-06f);  // |al - alpha_ref| / al <= 2^-21 s + 2^-19
+    // |al - alpha_ref| / al <= 2^-21 s (Q) + 2^-20 (exp2 approx, log2e product, sigma, product)
+    rel = fmaf(s, 4.7683716e-07f, 9.5367432e-07f);
     if (qf > g.qcull + tol) return kCulled;
     if (qf >= g.qcull - tol) return kUnsure;
     if (qf <= g.qclamp + tol) {
@@ -301,7 +310,8 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
     s.last = j + 1;
     // relative error bound of T: error of om plus one rounding of the product
     s.eps += fmaf(__fdividef(al, om), rel, 1.2e-7f);
-    const float m = fmaf(4.f, s.eps, 2e-6f);
+    // T = T_exact (1 +- eps) to first order; 1e-4f and the float compare add < 1e-7
+    const float m = fmaf(1.0625f, s.eps, 2e-7f);
     const float T = s.T;
     if (T < kTermF * (1.f - m)) {
         active = false;  // certainly terminated (_kernels.py:110-111)
@@ -379,18 +389,25 @@ __global__ void __launch_bounds__(kBlock, 3) raster_fwd_kernel(RasterArgs p) {
     }
 }
 
-// Exact re-render of flagged pixels: one warp per pixel.  Lanes screen 32
-// candidates at a time with the certified float32 test and run the exact
-// float64 reference test only where it cannot decide; the warp then walks the
-// contributors in order with the reference's float64 accumulation
-// `acc = acc + alpha * (1 - acc)` deciding termination (_kernels.py:105-111),
-// and the same float32 (or TRAIN float64) value recurrences as the main pass.
+// Exact re-render of flagged pixels: one CTA per pixel.  The CTA's 256
+// threads evaluate up to kFixSeg candidates of the tile list in parallel
+// (certified float32 screen, exact float64 reference test for the survivors)
+// into shared memory; warp 0 then walks them in list order, running the
+// reference's float64 accumulation `acc = acc + alpha * (1 - acc)` for the
+// termination decision (_kernels.py:105-111) and the same float32 (or TRAIN
+// float64) value recurrences as the main pass.
+constexpr int kFixSeg = 1024;
+
 template <bool TRAIN>
 __global__ void __launch_bounds__(256) fixup_kernel(RasterArgs p) {
-    const int lane = threadIdx.x & 31;
+    __shared__ double s_a64[kFixSeg];
+    __shared__ float4 s_val[kFixSeg];    // al, ax, ay, axy
+    __shared__ float4 s_col[kFixSeg];
+    __shared__ int8_t s_st[kFixSeg];
+    __shared__ int s_done;
+    const int tid = threadIdx.x, lane = tid & 31;
     const uint32_t nfix = p.counters[2];
-    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nfix;
-         w += (gridDim.x * blockDim.x) >> 5) {
+    for (uint32_t w = blockIdx.x; w < nfix; w += gridDim.x) {
         const uint32_t pix = p.fixup[w];
         const int px = (int)(pix % (uint32_t)p.width), py = (int)(pix / (uint32_t)p.width);
         const int tile = (py / kTile) * p.ntx + px / kTile;
@@ -400,51 +417,53 @@ __global__ void __launch_bounds__(256) fixup_kernel(RasterArgs p) {
         s.init();
         s.last = start;
         double acc = 0.0;
-        bool done = false;
-        for (uint32_t base = start; base < end && !done; base += 32) {
-            const uint32_t j = base + lane;
-            int st = kCulled;
-            double a64 = 0.0;
-            float al = 0.f, gax = 0.f, gay = 0.f, gaxy = 0.f, rel;
-            float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (j < end) {
-                const uint32_t r = p.ranks[j];
+        if (tid == 0) s_done = 0;
+        for (uint32_t seg = start; seg < end; seg += kFixSeg) {
+            const int nseg = (int)min((uint32_t)kFixSeg, end - seg);
+            for (int i = tid; i < nseg; i += blockDim.x) {
+                const uint32_t r = p.ranks[seg + i];
                 const PackF g = p.pack[r];
-                st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
+                float al = 0.f, gax = 0.f, gay = 0.f, gaxy = 0.f, rel;
+                double a64 = 0.0;
+                int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
                 if (st != kCulled) {
-                    // the exact alpha drives the termination chain
-                    st = eval_exact(p.sc, p.vc, p.bboxes, r, px, py, &a64);
-                    if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
-                    col = p.sc.color[r];
+                    st = eval_exact_inl(p.sc, p.vc, p.bboxes, r, px, py, &a64);
+                    if (st != kCulled) {
+                        canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
+                        s_col[i] = p.sc.color[r];
+                    }
                 }
+                s_st[i] = (int8_t)st;
+                s_a64[i] = a64;
+                s_val[i] = make_float4(al, gax, gay, gaxy);
             }
-            uint32_t bits = __ballot_sync(0xffffffffu, st != kCulled);
-            while (bits) {
-                const int k = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const double ak = __shfl_sync(0xffffffffu, a64, k);
-                const int stk = __shfl_sync(0xffffffffu, st, k);
-                const float alk = __shfl_sync(0xffffffffu, al, k);
-                const float axk = __shfl_sync(0xffffffffu, gax, k);
-                const float ayk = __shfl_sync(0xffffffffu, gay, k);
-                const float axyk = __shfl_sync(0xffffffffu, gaxy, k);
-                float4 ck;
-                ck.x = __shfl_sync(0xffffffffu, col.x, k);
-                ck.y = __shfl_sync(0xffffffffu, col.y, k);
-                ck.z = __shfl_sync(0xffffffffu, col.z, k);
-                ck.w = 0.f;
-                const float om = stk == kClamped ? 1.0e-3f : 1.f - alk;
-                s.add(alk, axk, ayk, axyk, om, ck);
-                s.last = base + k + 1;
-                const double t = __dsub_rn(1.0, acc);
-                acc = __dadd_rn(acc, __dmul_rn(ak, t));
-                if (__dsub_rn(1.0, acc) < kEarlyTerm) {
-                    done = true;
-                    break;
+            __syncthreads();
+            if (tid < 32) {
+                bool done = false;
+                for (int c0 = 0; c0 < nseg && !done; c0 += 32) {
+                    uint32_t bits = __ballot_sync(0xffffffffu, c0 + lane < nseg && s_st[c0 + lane] != kCulled);
+                    while (bits) {
+                        const int k = c0 + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const float4 v = s_val[k];
+                        const float om = s_st[k] == kClamped ? 1.0e-3f : 1.f - v.x;
+                        s.add(v.x, v.y, v.z, v.w, om, s_col[k]);
+                        s.last = seg + k + 1;
+                        const double t = __dsub_rn(1.0, acc);
+                        acc = __dadd_rn(acc, __dmul_rn(s_a64[k], t));
+                        if (__dsub_rn(1.0, acc) < kEarlyTerm) {
+                            done = true;
+                            break;
+                        }
+                    }
                 }
+                if (lane == 0 && done) s_done = 1;
             }
+            __syncthreads();
+            if (s_done) break;
         }
-        if (lane == 0) write_pixel<TRAIN>(p, px, py, s);
+        if (tid == 0) write_pixel<TRAIN>(p, px, py, s);
+        __syncthreads();
     }
 }
 
@@ -474,10 +493,10 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
     int ntiles = L.ntx * L.nty;
     if (train) {
         raster_fwd_kernel<true><<<ntiles, kBlock, 0, stream>>>(a); note_launch();
-        fixup_kernel<true><<<148 * 2, 256, 0, stream>>>(a); note_launch();
+        fixup_kernel<true><<<148 * 4, 256, 0, stream>>>(a); note_launch();
     } else {
         raster_fwd_kernel<false><<<ntiles, kBlock, 0, stream>>>(a); note_launch();
-        fixup_kernel<false><<<148 * 2, 256, 0, stream>>>(a); note_launch();
+        fixup_kernel<false><<<148 * 4, 256, 0, stream>>>(a); note_launch();
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
