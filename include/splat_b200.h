@@ -132,8 +132,12 @@ int splat_view_pack64(const void *scene_const, int64_t n, const splat_view_t *vi
 /* ---- spline upscaler ----------------------------------------------------
  * upscale_spline (spline.py:162-178): (H,W,4,3) gradient planes -> (Ho,Wo,3).
  * upscale_backward (spline.py:191-243): (Ho,Wo,3) adjoint -> (H,W,4,3). */
+size_t splat_upscale_plan_bytes(int in_w, int in_h, int out_w, int out_h);
+/* Per-axis maps (floor(s), Hermite weights) for one (in, out) size pair;
+ * reusable by every upscale of that size (spline.py:102-112). */
+int splat_upscale_plan(int in_w, int in_h, int out_w, int out_h, void *plan, void *stream);
 int splat_upscale_forward(const float *src, int in_w, int in_h, float *out, int out_w, int out_h,
-                          int clamp, void *stream);
+                          int clamp, const void *plan, void *stream);
 int splat_upscale_backward(const float *adjoint, int out_w, int out_h, float *dsrc, int in_w,
                            int in_h, void *stream);
 /* fd_gradients / fd_gradients_backward (spline.py:274-297). */

@@ -64,7 +64,9 @@ SIGNATURES = {
     "splat_rasterize": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
                               ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_view_pack64": (I32, [P, I64, ctypes.POINTER(ViewT), P, P]),
-    "splat_upscale_forward": (I32, [P, I32, I32, P, I32, I32, I32, P]),
+    "splat_upscale_plan_bytes": (SZ, [I32, I32, I32, I32]),
+    "splat_upscale_plan": (I32, [I32, I32, I32, I32, P, P]),
+    "splat_upscale_forward": (I32, [P, I32, I32, P, I32, I32, I32, P, P]),
     "splat_upscale_backward": (I32, [P, I32, I32, P, I32, I32, P]),
     "splat_fd_gradients": (I32, [P, I32, I32, P, P]),
     "splat_fd_gradients_backward": (I32, [P, I32, I32, P, P, P]),

@@ -27,7 +27,9 @@ int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaSt
 bool sorted_in_alt(int ntiles);
 int launch_pack64(const SceneConst& sc, const ViewConst& vc, double* out, cudaStream_t stream);
 int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
-                         int clamp, cudaStream_t stream);
+                         int clamp, const void* plan, cudaStream_t stream);
+size_t upscale_plan_bytes_impl(int out_w, int out_h);
+int upscale_plan_impl(int in_w, int in_h, int out_w, int out_h, void* plan, cudaStream_t stream);
 int upscale_backward_impl(const float* adj, int out_w, int out_h, float* dsrc, int in_w, int in_h,
                           cudaStream_t stream);
 int fd_forward_impl(const float* img, int w, int h, float* planes, cudaStream_t stream);
@@ -142,12 +144,26 @@ int splat_rasterize(const void* scene_const, int64_t n, const splat_view_t* view
                                  (char*)workspace, *out, train != 0, (cudaStream_t)stream);
 }
 
-int splat_upscale_forward(const float* src, int in_w, int in_h, float* out, int out_w, int out_h, int clamp,
-                          void* stream) {
+size_t splat_upscale_plan_bytes(int in_w, int in_h, int out_w, int out_h) {
+    (void)in_w;
+    (void)in_h;
+    return upscale_plan_bytes_impl(out_w, out_h);
+}
+
+int splat_upscale_plan(int in_w, int in_h, int out_w, int out_h, void* plan, void* stream) {
     if (in_w <= 0 || in_h <= 0) return set_error(SPLAT_ERR_DIMENSION, "empty source image");
     if (out_w < in_w || out_h < in_h)
         return set_error(SPLAT_ERR_SCALE, "output must be at least source size");
-    return upscale_forward_impl(src, in_w, in_h, out, out_w, out_h, clamp, (cudaStream_t)stream);
+    return upscale_plan_impl(in_w, in_h, out_w, out_h, plan, (cudaStream_t)stream);
+}
+
+int splat_upscale_forward(const float* src, int in_w, int in_h, float* out, int out_w, int out_h, int clamp,
+                          const void* plan, void* stream) {
+    if (in_w <= 0 || in_h <= 0) return set_error(SPLAT_ERR_DIMENSION, "empty source image");
+    if (out_w < in_w || out_h < in_h)
+        return set_error(SPLAT_ERR_SCALE, "output must be at least source size");
+    if (!plan) return set_error(SPLAT_ERR_PARAMETER, "upscale plan required (splat_upscale_plan)");
+    return upscale_forward_impl(src, in_w, in_h, out, out_w, out_h, clamp, plan, (cudaStream_t)stream);
 }
 
 int splat_upscale_backward(const float* adjoint, int out_w, int out_h, float* dsrc, int in_w, int in_h,

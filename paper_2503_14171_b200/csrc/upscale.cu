@@ -28,8 +28,7 @@ namespace splat {
 
 namespace {
 
-constexpr int kUpRows = 8;
-constexpr int kUpCols = 128;
+constexpr int kUpRows = 16;
 
 struct AxisMap {
     int i0;        // floor(s)
@@ -57,118 +56,309 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// ---- upscale plan: per-axis maps computed once per (in, out) size ------------------------
+// Table entry for output index u: i0 = floor(s) and the 4 Hermite weights,
+// s = (u + .5) / (n_out / n_in) - .5 in float64 exactly as numpy computes it.
+// Tables are padded to a multiple of the tile size (tail entries repeat the
+// last index) so every tile's slice can be bulk-copied without bounds checks.
+constexpr int kPlanPad = 256;
+
+__global__ void plan_kernel(int n_out, int n_pad, double scale, int* __restrict__ i0,
+                            float4* __restrict__ w) {
+    int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n_pad) return;
+    AxisMap m = axis_map(min(u, n_out - 1), scale);
+    i0[u] = m.i0;
+    w[u] = make_float4(m.h[0], m.h[1], m.h[2], m.h[3]);
+}
+
+struct PlanView {
+    const int* ci0;
+    const float4* cw;
+    const int* ri0;
+    const float4* rw;
+};
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+// Persistent upscaler.  Each CTA walks output tiles of kUpRows x tile_c
+// pixels; for tile i+1 it issues the TMA bulk copies (source rows, column and
+// row maps) into the other shared-memory stage before computing tile i, so
+// HBM reads overlap the arithmetic and the 16-byte output stores.
 __global__ void __launch_bounds__(256) upscale_fwd_kernel(const float* __restrict__ src, int in_w,
                                                           int in_h, float* __restrict__ out, int out_w,
-                                                          int out_h, double scale_x, double scale_y,
-                                                          int clamp, int span_cols, int span_rows) {
+                                                          int out_h, int clamp, PlanView plan, int tile_c,
+                                                          int span_c, int span_r) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ AxisMap s_cmap[kUpCols];
-    __shared__ AxisMap s_rmap[kUpRows];
-    __shared__ int s_box[4];
-    __shared__ __align__(8) unsigned long long s_bar;
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ int s_box[2][4];
 
     const int tid = threadIdx.x;
-    const int U0 = blockIdx.x * kUpCols, V0 = blockIdx.y * kUpRows;
-    float* s_src = reinterpret_cast<float*>(smem);                 // span_rows x span_cols x 12
-    float* s_g = s_src + (size_t)span_rows * span_cols * 12;       // kUpRows x span_cols x 6
-
-    if (tid < kUpCols) {
-        int u = min(U0 + tid, out_w - 1);
-        s_cmap[tid] = axis_map(u, scale_x);
-    } else if (tid < kUpCols + kUpRows) {
-        int v = min(V0 + tid - kUpCols, out_h - 1);
-        s_rmap[tid - kUpCols] = axis_map(v, scale_y);
-    }
+    const int ntx = (out_w + tile_c - 1) / tile_c;
+    const int nty = (out_h + kUpRows - 1) / kUpRows;
+    const int ntiles = ntx * nty;
+    const size_t src_floats = (size_t)span_r * span_c * 12;
+    float* const s_src0 = reinterpret_cast<float*>(smem);                 // 2 stages of span_r x span_c x 12
+    float* const s_g = s_src0 + 2 * src_floats;                           // kUpRows x span_c x 6
+    // per-stage map slices: [cw tile_c float4][rw kUpRows float4][ci0 tile_c int][ri0 kUpRows int]
+    unsigned char* const s_map0 = reinterpret_cast<unsigned char*>(s_g + (size_t)kUpRows * span_c * 6);
+    const size_t map_bytes = (size_t)tile_c * 20 + kUpRows * 20;
+#define STAGE_SRC(b) (s_src0 + (size_t)(b) * src_floats)
+#define STAGE_CW(b) reinterpret_cast<float4*>(s_map0 + (size_t)(b) * map_bytes)
+#define STAGE_RW(b) reinterpret_cast<float4*>(s_map0 + (size_t)(b) * map_bytes + (size_t)tile_c * 16)
+#define STAGE_CI(b) reinterpret_cast<int*>(s_map0 + (size_t)(b) * map_bytes + (size_t)tile_c * 16 + kUpRows * 16)
+#define STAGE_RI(b) reinterpret_cast<int*>(s_map0 + (size_t)(b) * map_bytes + (size_t)tile_c * 20 + kUpRows * 16)
     if (tid == 0) {
-        int ulast = min(U0 + kUpCols, out_w) - 1, vlast = min(V0 + kUpRows, out_h) - 1;
-        AxisMap a = axis_map(U0, scale_x), b = axis_map(ulast, scale_x);
-        AxisMap c = axis_map(V0, scale_y), d = axis_map(vlast, scale_y);
-        s_box[0] = clampi(a.i0, 0, in_w - 1);
-        s_box[1] = clampi(b.i0 + 1, 0, in_w - 1);
-        s_box[2] = clampi(c.i0, 0, in_h - 1);
-        s_box[3] = clampi(d.i0 + 1, 0, in_h - 1);
-        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[0])));
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    const int x0 = s_box[0], ncols = s_box[1] - s_box[0] + 1;
-    const int y0 = s_box[2], nrows = s_box[3] - s_box[2] + 1;
 
-    // TMA bulk copies: one contiguous source row segment (ncols * 48 B) per row
-    if (tid == 0) {
-        uint32_t bytes = (uint32_t)(ncols * 48) * (uint32_t)nrows;
-        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
+    // thread 0: compute the source box of tile t and launch its copies into stage b
+    auto issue = [&](int t, int b) {
+        const int U0 = (t % ntx) * tile_c, V0 = (t / ntx) * kUpRows;
+        const int ulast = min(U0 + tile_c, out_w) - 1, vlast = min(V0 + kUpRows, out_h) - 1;
+        const int x0 = clampi(plan.ci0[U0], 0, in_w - 1), x1 = clampi(plan.ci0[ulast] + 1, 0, in_w - 1);
+        const int y0 = clampi(plan.ri0[V0], 0, in_h - 1), y1 = clampi(plan.ri0[vlast] + 1, 0, in_h - 1);
+        s_box[b][0] = x0;
+        s_box[b][1] = x1 - x0 + 1;
+        s_box[b][2] = y0;
+        s_box[b][3] = y1 - y0 + 1;
+        const uint32_t row_bytes = (uint32_t)(x1 - x0 + 1) * 48u;
+        const uint32_t bytes = row_bytes * (uint32_t)(y1 - y0 + 1) + (uint32_t)tile_c * 20u + kUpRows * 20u;
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar[b])),
                      "r"(bytes)
                      : "memory");
-        for (int r = 0; r < nrows; ++r) {
-            const float* g = src + ((size_t)(y0 + r) * in_w + x0) * 12;
-            float* d = s_src + (size_t)r * span_cols * 12;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    smem_u32(d)),
-                "l"(g), "r"((uint32_t)(ncols * 48)), "r"(smem_u32(&s_bar))
-                : "memory");
-        }
-    }
-    // wait for the transaction bytes (phase 0)
-    {
-        uint32_t done = 0;
-        while (!done) {
-            asm volatile(
-                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
-                : "=r"(done)
-                : "r"(smem_u32(&s_bar))
-                : "memory");
-        }
-    }
+        for (int r = 0; r <= y1 - y0; ++r)
+            bulk_copy(STAGE_SRC(b) + (size_t)r * span_c * 12, src + ((size_t)(y0 + r) * in_w + x0) * 12,
+                      row_bytes, &s_bar[b]);
+        bulk_copy(STAGE_CW(b), plan.cw + U0, (uint32_t)tile_c * 16u, &s_bar[b]);
+        bulk_copy(STAGE_CI(b), plan.ci0 + U0, (uint32_t)tile_c * 4u, &s_bar[b]);
+        bulk_copy(STAGE_RW(b), plan.rw + V0, kUpRows * 16u, &s_bar[b]);
+        bulk_copy(STAGE_RI(b), plan.ri0 + V0, kUpRows * 4u, &s_bar[b]);
+    };
 
-    // y pass: G[v][x] = (value-in-x, slope-in-x) along output row v
-    const int nv = min(kUpRows, out_h - V0);
-    for (int e = tid; e < nv * ncols; e += blockDim.x) {
-        int v = e / ncols, x = e - v * ncols;
-        const AxisMap& rm = s_rmap[v];
-        int ra = clampi(rm.i0, 0, in_h - 1) - y0, rb = clampi(rm.i0 + 1, 0, in_h - 1) - y0;
-        const float* pa = s_src + ((size_t)ra * span_cols + x) * 12;
-        const float* pb = s_src + ((size_t)rb * span_cols + x) * 12;
-        float* gd = s_g + ((size_t)v * span_cols + x) * 6;
+    int t = blockIdx.x;
+    if (t < ntiles && tid == 0) issue(t, 0);
+    uint32_t phases = 0u;  // bit b = parity of stage b's next completion
+    for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
+        const int tn = t + gridDim.x;
+        if (tn < ntiles && tid == 0) issue(tn, b ^ 1);
+        mbar_wait(&s_bar[b], (phases >> b) & 1u);
+        phases ^= 1u << b;
+        const int U0 = (t % ntx) * tile_c, V0 = (t / ntx) * kUpRows;
+        const int x0 = s_box[b][0], ncols = s_box[b][1], y0 = s_box[b][2];
+        const int nv = min(kUpRows, out_h - V0);
+        const float* sb = STAGE_SRC(b);
+        const float4* s_rwb = STAGE_RW(b);
+        const int* s_rib = STAGE_RI(b);
+        const float4* s_cwb = STAGE_CW(b);
+        const int* s_cib = STAGE_CI(b);
+        // y pass: G[v][x] = (value-in-x, slope-in-x) of output row v at source column x.
+        // Source records (48 B) are read as 3 x LDS.128 and G records (24 B) written as
+        // 3 x STS.64: both strides are bank-conflict free.
+        for (int e = tid; e < nv * ncols; e += blockDim.x) {
+            const int v = e / ncols, x = e - v * ncols;
+            const float4 h = s_rwb[v];
+            const int ri = s_rib[v];
+            const int ra = clampi(ri, 0, in_h - 1) - y0, rb = clampi(ri + 1, 0, in_h - 1) - y0;
+            const float4* pa = reinterpret_cast<const float4*>(sb + ((size_t)ra * span_c + x) * 12);
+            const float4* pb = reinterpret_cast<const float4*>(sb + ((size_t)rb * span_c + x) * 12);
+            const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];
+            const float4 b0 = pb[0], b1 = pb[1], b2 = pb[2];
+            // record = [f0 f1 f2 fx0 | fx1 fx2 fy0 fy1 | fy2 fxy0 fxy1 fxy2]
+            const float fa[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+            const float fb[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+            float g[6];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            // value planes: f and f_y ; slope planes: f_x and f_xy
-            gd[c] = rm.h[0] * pa[c] + rm.h[1] * pb[c] + rm.h[2] * pa[6 + c] + rm.h[3] * pb[6 + c];
-            gd[3 + c] = rm.h[0] * pa[3 + c] + rm.h[1] * pb[3 + c] + rm.h[2] * pa[9 + c] + rm.h[3] * pb[9 + c];
+            for (int c = 0; c < 3; ++c) {
+                g[c] = fmaf(h.x, fa[c], fmaf(h.y, fb[c], fmaf(h.z, fa[6 + c], h.w * fb[6 + c])));
+                g[3 + c] = fmaf(h.x, fa[3 + c], fmaf(h.y, fb[3 + c], fmaf(h.z, fa[9 + c], h.w * fb[9 + c])));
+            }
+            float2* gd = reinterpret_cast<float2*>(s_g + ((size_t)v * span_c + x) * 6);
+            gd[0] = make_float2(g[0], g[1]);
+            gd[1] = make_float2(g[2], g[3]);
+            gd[2] = make_float2(g[4], g[5]);
         }
+        __syncthreads();
+        // x pass: 4 consecutive output pixels per thread and step
+        const int groups_per_row = tile_c / 4;
+        const int nu = min(tile_c, out_w - U0);
+        for (int e = tid; e < nv * groups_per_row; e += blockDim.x) {
+            const int v = e / groups_per_row, ug = (e - v * groups_per_row) * 4;
+            if (ug >= nu) continue;
+            float o[12];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int uu = min(ug + i, nu - 1);
+                const float4 h = s_cwb[uu];
+                const int ci = s_cib[uu];
+                const int xa = clampi(ci, 0, in_w - 1) - x0, xb = clampi(ci + 1, 0, in_w - 1) - x0;
+                const float2* ga = reinterpret_cast<const float2*>(s_g + ((size_t)v * span_c + xa) * 6);
+                const float2* gb = reinterpret_cast<const float2*>(s_g + ((size_t)v * span_c + xb) * 6);
+                const float2 a0 = ga[0], a1 = ga[1], a2 = ga[2], b0 = gb[0], b1 = gb[1], b2 = gb[2];
+                const float A[6] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y};
+                const float B[6] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y};
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    float val = fmaf(h.x, A[c], fmaf(h.y, B[c], fmaf(h.z, A[3 + c], h.w * B[3 + c])));
+                    if (clamp) val = fminf(fmaxf(val, 0.f), 1.f);
+                    o[3 * i + c] = val;
+                }
+            }
+            float* dst = out + ((size_t)(V0 + v) * out_w + U0 + ug) * 3;
+            if (ug + 3 < nu && (out_w & 3) == 0) {
+                float4* d4 = reinterpret_cast<float4*>(dst);
+                __stcs(d4, make_float4(o[0], o[1], o[2], o[3]));
+                __stcs(d4 + 1, make_float4(o[4], o[5], o[6], o[7]));
+                __stcs(d4 + 2, make_float4(o[8], o[9], o[10], o[11]));
+            } else {
+                for (int i = 0; i < 4 && ug + i < nu; ++i)
+                    for (int c = 0; c < 3; ++c) dst[3 * i + c] = o[3 * i + c];
+            }
+        }
+        __syncthreads();
+    }
+#undef STAGE_SRC
+#undef STAGE_CW
+#undef STAGE_RW
+#undef STAGE_CI
+#undef STAGE_RI
+}
+
+// ---- integer factors (x2, x4: the benchmark configurations) ------------------------------
+// With out = F * in exactly, output column u = F m + j maps to a fixed phase
+// (i0 - m, t) that repeats every F pixels, so the Hermite weights are per-phase
+// constants and no per-column maps are needed.  A CTA computes a 16-row x
+// (64 F)-column output tile: one TMA bulk copy per source row into shared
+// memory, the y pass G[v][x] for the tile's source columns, then each thread
+// emits 4 consecutive pixels of a row (3 x 16-byte streaming stores) from the
+// G records of the F-aligned cells they fall in.  Clamping to [0, 1] is the
+// .sat modifier of the last FMA (spline.py:178).
+
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {
+    float r;
+    asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+__host__ __device__ constexpr int int_tile_cols(int F) { return 64 * F; }
+
+template <int F>
+__global__ void __launch_bounds__(256) upscale_int_kernel(const float* __restrict__ src, int in_w, int in_h,
+                                                          float* __restrict__ out, int out_w, int out_h,
+                                                          int clamp, float4 hw0, float4 hw1, float4 hw2,
+                                                          float4 hw3, int span_c, int span_r) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar;
+    constexpr int TC = int_tile_cols(F);
+    const int tid = threadIdx.x;
+    const int U0 = blockIdx.x * TC, V0 = blockIdx.y * kUpRows;
+    // source columns m(U0) - 1 .. m(U0 + TC - 1) + 1 where cell m = floor((u + .5)/F - .5)
+    const int cx0 = U0 / F - 1, cy0 = V0 / F - 1;
+    const int x0 = max(cx0, 0), x1 = min((U0 + TC) / F, in_w - 1);
+    const int y0 = max(cy0, 0), y1 = min((V0 + kUpRows) / F, in_h - 1);
+    const int ncols = x1 - x0 + 1, nrows = y1 - y0 + 1;
+    float* s_src = reinterpret_cast<float*>(smem);
+    float* s_g = s_src + (size_t)span_r * span_c * 12;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t row_bytes = (uint32_t)ncols * 48u;
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
+                     "r"(row_bytes * (uint32_t)nrows)
+                     : "memory");
+        for (int r = 0; r < nrows; ++r)
+            bulk_copy(s_src + (size_t)r * span_c * 12, src + ((size_t)(y0 + r) * in_w + x0) * 12, row_bytes,
+                      &s_bar);
     }
     __syncthreads();
-
-    // x pass: each thread writes 4 consecutive output pixels of one row
-    const int v = tid >> 5;
-    const int ug = (tid & 31) * 4;
-    if (v < nv) {
-        const int vrow = V0 + v;
+    mbar_wait(&s_bar, 0);
+    // Hermite weights of phase j (F <= 4), selected without local memory
+    auto phase_w = [&](int j) { return j == 0 ? hw0 : (j == 1 ? hw1 : (j == 2 ? hw2 : hw3)); };
+    // y pass over the tile rows
+    const int nv = min(kUpRows, out_h - V0);
+    // G columns are indexed by cell column relative to cx0 (clamped reads keep edges right)
+    const int gcols = TC / F + 2;
+    for (int e = tid; e < nv * gcols; e += blockDim.x) {
+        const int v = e / gcols, gc = e - v * gcols;
+        const int vv = V0 + v;
+        const int jy = (vv + F / 2) % F;                 // phase of this output row
+        const int iy = (vv + F / 2) / F - 1;             // floor((v + .5)/F - .5)
+        const float4 h = phase_w(jy);
+        const int ra = clampi(iy, 0, in_h - 1) - y0, rb = clampi(iy + 1, 0, in_h - 1) - y0;
+        const int xc = clampi(cx0 + gc, 0, in_w - 1) - x0;
+        const float4* pa = reinterpret_cast<const float4*>(s_src + ((size_t)ra * span_c + xc) * 12);
+        const float4* pb = reinterpret_cast<const float4*>(s_src + ((size_t)rb * span_c + xc) * 12);
+        const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];
+        const float4 b0 = pb[0], b1 = pb[1], b2 = pb[2];
+        const float fa[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+        const float fb[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+        float g[6];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            g[c] = fmaf(h.x, fa[c], fmaf(h.y, fb[c], fmaf(h.z, fa[6 + c], h.w * fb[6 + c])));
+            g[3 + c] = fmaf(h.x, fa[3 + c], fmaf(h.y, fb[3 + c], fmaf(h.z, fa[9 + c], h.w * fb[9 + c])));
+        }
+        float2* gd = reinterpret_cast<float2*>(s_g + ((size_t)v * gcols + gc) * 6);
+        gd[0] = make_float2(g[0], g[1]);
+        gd[1] = make_float2(g[2], g[3]);
+        gd[2] = make_float2(g[4], g[5]);
+    }
+    __syncthreads();
+    // x pass: thread -> 4 consecutive pixels u = U0 + 4k .. +3 of row v
+    constexpr int GPR = TC / 4;  // groups per row
+    const int nu = min(TC, out_w - U0);
+    for (int e = tid; e < nv * GPR; e += blockDim.x) {
+        const int v = e / GPR, ug = (e - v * GPR) * 4;
+        if (ug >= nu) continue;
         float o[12];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const AxisMap& cm = s_cmap[ug + i];
-            int xa = clampi(cm.i0, 0, in_w - 1) - x0, xb = clampi(cm.i0 + 1, 0, in_w - 1) - x0;
-            const float* ga = s_g + ((size_t)v * span_cols + xa) * 6;
-            const float* gb = s_g + ((size_t)v * span_cols + xb) * 6;
+            // U0 + ug is a multiple of 4 (hence of F): the phase is static per i
+            const int jx = (i + F / 2) % F;
+            const int ix = (U0 + ug) / F + (i + F / 2) / F - 1;   // cell column of this pixel
+            const float4 h = jx == 0 ? hw0 : (jx == 1 ? hw1 : (jx == 2 ? hw2 : hw3));
+            const int gca = ix - cx0, gcb = gca + 1;      // G columns of the two corners
+            const float2* ga = reinterpret_cast<const float2*>(s_g + ((size_t)v * gcols + gca) * 6);
+            const float2* gb = reinterpret_cast<const float2*>(s_g + ((size_t)v * gcols + gcb) * 6);
+            const float2 a0 = ga[0], a1 = ga[1], a2 = ga[2], b0 = gb[0], b1 = gb[1], b2 = gb[2];
+            const float A[6] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y};
+            const float B[6] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y};
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                float val = cm.h[0] * ga[c] + cm.h[1] * gb[c] + cm.h[2] * ga[3 + c] + cm.h[3] * gb[3 + c];
-                if (clamp) val = fminf(fmaxf(val, 0.f), 1.f);
-                o[3 * i + c] = val;
+                const float part = fmaf(h.y, B[c], fmaf(h.z, A[3 + c], h.w * B[3 + c]));
+                o[3 * i + c] = clamp ? fma_sat(h.x, A[c], part) : fmaf(h.x, A[c], part);
             }
         }
-        const int u = U0 + ug;
-        float* dst = out + ((size_t)vrow * out_w + u) * 3;
-        if (u + 3 < out_w && (out_w & 3) == 0) {
+        float* dst = out + ((size_t)(V0 + v) * out_w + U0 + ug) * 3;
+        if (ug + 3 < nu && (out_w & 3) == 0) {
             float4* d4 = reinterpret_cast<float4*>(dst);
-            d4[0] = make_float4(o[0], o[1], o[2], o[3]);
-            d4[1] = make_float4(o[4], o[5], o[6], o[7]);
-            d4[2] = make_float4(o[8], o[9], o[10], o[11]);
+            __stcs(d4, make_float4(o[0], o[1], o[2], o[3]));
+            __stcs(d4 + 1, make_float4(o[4], o[5], o[6], o[7]));
+            __stcs(d4 + 2, make_float4(o[8], o[9], o[10], o[11]));
         } else {
-            for (int i = 0; i < 4 && u + i < out_w; ++i)
+            for (int i = 0; i < 4 && ug + i < nu; ++i)
                 for (int c = 0; c < 3; ++c) dst[3 * i + c] = o[3 * i + c];
         }
     }
@@ -363,25 +553,106 @@ __global__ void fd_bwd_kernel(const float* __restrict__ dplanes, const float* __
 
 }  // namespace
 
-int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
-                         int clamp, cudaStream_t stream) {
-    if (out_w <= 0 || out_h <= 0) return SPLAT_OK;
-    double sx = (double)out_w / (double)in_w, sy = (double)out_h / (double)in_h;
-    int span_cols = (int)ceil(kUpCols / sx) + 3;
-    int span_rows = (int)ceil(kUpRows / sy) + 3;
-    if (span_cols > in_w) span_cols = in_w;
-    if (span_rows > in_h) span_rows = in_h;
-    size_t smem = (size_t)span_rows * span_cols * 12 * 4 + (size_t)kUpRows * span_cols * 6 * 4;
+size_t upscale_plan_bytes_impl(int out_w, int out_h) {
+    size_t pw = (size_t)((out_w + kPlanPad - 1) / kPlanPad) * kPlanPad;
+    size_t ph = (size_t)((out_h + kPlanPad - 1) / kPlanPad) * kPlanPad;
+    return (pw + ph) * 20 + 64;
+}
+
+static PlanView plan_view(const void* plan, int out_w) {
+    size_t pw = (size_t)((out_w + kPlanPad - 1) / kPlanPad) * kPlanPad;
+    const char* b = (const char*)plan;
+    PlanView v;
+    v.cw = (const float4*)b;
+    v.ci0 = (const int*)(b + pw * 16);
+    v.rw = (const float4*)(b + pw * 20);
+    return v;
+}
+
+int upscale_plan_impl(int in_w, int in_h, int out_w, int out_h, void* plan, cudaStream_t stream) {
+    int pw = (out_w + kPlanPad - 1) / kPlanPad * kPlanPad;
+    int ph = (out_h + kPlanPad - 1) / kPlanPad * kPlanPad;
+    char* b = (char*)plan;
+    float4* cw = (float4*)b;
+    int* ci0 = (int*)(b + (size_t)pw * 16);
+    float4* rw = (float4*)(b + (size_t)pw * 20);
+    int* ri0 = (int*)(b + (size_t)pw * 20 + (size_t)ph * 16);
+    plan_kernel<<<ceil_div(pw, 256), 256, 0, stream>>>(out_w, pw, (double)out_w / (double)in_w, ci0, cw); note_launch();
+    plan_kernel<<<ceil_div(ph, 256), 256, 0, stream>>>(out_h, ph, (double)out_h / (double)in_h, ri0, rw); note_launch();
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
+
+template <int F>
+static int upscale_int_launch(const float* src, int in_w, int in_h, float* out, int out_w, int out_h, int clamp,
+                              cudaStream_t stream) {
+    constexpr int TC = int_tile_cols(F);
+    const int span_c = TC / F + 3, span_r = kUpRows / F + 3;
+    const size_t smem = (size_t)span_r * span_c * 48 + (size_t)kUpRows * (TC / F + 2) * 24;
     static int configured = 0;
     if (!configured) {
-        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_fwd_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_int_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem));
         configured = 1;
     }
-    if (smem > 200 * 1024) return set_error(SPLAT_ERR_DIMENSION, "upscale tile exceeds shared memory");
-    dim3 grid(ceil_div(out_w, kUpCols), ceil_div(out_h, kUpRows));
-    upscale_fwd_kernel<<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h, sx, sy, clamp,
-                                                    span_cols, span_rows); note_launch();
+    // Hermite weights of the F phases: t_j = (j + .5) / F - .5 + (j < F/2 ? 1 : 0)
+    float4 hw[4];
+    for (int j = 0; j < 4; ++j) {
+        double t = j < F ? ((double)j + 0.5) / F - 0.5 + (j < F / 2 ? 1.0 : 0.0) : 0.0;
+        // phase j is defined by (u + F/2) % F; recover t from s = (u+.5)/F - .5
+        if (j < F) {
+            int u = (j - F / 2 + F) % F + F;  // any u with that phase (>= 0)
+            double s = ((double)u + 0.5) / F - 0.5;
+            t = s - floor(s);
+        }
+        double t2 = t * t, t3 = t2 * t;
+        hw[j] = make_float4((float)(1.0 - 3.0 * t2 + 2.0 * t3), (float)(3.0 * t2 - 2.0 * t3),
+                            (float)(t - 2.0 * t2 + t3), (float)(t3 - t2));
+    }
+    dim3 grid(ceil_div(out_w, TC), ceil_div(out_h, kUpRows));
+    upscale_int_kernel<F><<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h, clamp, hw[0], hw[1],
+                                                       hw[2], hw[3], span_c, span_r); note_launch();
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
+
+int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
+                         int clamp, const void* plan, cudaStream_t stream) {
+    if (out_w <= 0 || out_h <= 0) return SPLAT_OK;
+    if (out_w == 4 * in_w && out_h == 4 * in_h)
+        return upscale_int_launch<4>(src, in_w, in_h, out, out_w, out_h, clamp, stream);
+    if (out_w == 2 * in_w && out_h == 2 * in_h)
+        return upscale_int_launch<2>(src, in_w, in_h, out, out_w, out_h, clamp, stream);
+    double sx = (double)out_w / (double)in_w, sy = (double)out_h / (double)in_h;
+    int tile_c = sx >= 4.0 ? 256 : (sx >= 2.0 ? 128 : 64);
+    int span_c = (int)ceil((tile_c - 1) / sx) + 3;
+    int span_r = (int)ceil((kUpRows - 1) / sy) + 3;
+    if (span_c > in_w) span_c = in_w;
+    if (span_r > in_h) span_r = in_h;
+    size_t smem = 2 * (size_t)span_r * span_c * 48 + (size_t)kUpRows * span_c * 24 +
+                  2 * ((size_t)tile_c * 20 + kUpRows * 20);
+    static int max_smem = 0;
+    if (!max_smem) {
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_fwd_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        max_smem = 220 * 1024;
+    }
+    if (smem > (size_t)max_smem) return set_error(SPLAT_ERR_DIMENSION, "upscale tile exceeds shared memory");
+    int per_sm = 0;
+    SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_fwd_kernel, 256, smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int ntiles = ceil_div(out_w, tile_c) * ceil_div(out_h, kUpRows);
+    int grid = per_sm * sms;
+    if (grid > ntiles) grid = ntiles;
+    if (grid < 1) grid = 1;
+    PlanView pv = plan_view(plan, out_w);
+    int pw = (out_w + kPlanPad - 1) / kPlanPad * kPlanPad;
+    int ph = (out_h + kPlanPad - 1) / kPlanPad * kPlanPad;
+    pv.ri0 = (const int*)((const char*)plan + (size_t)pw * 20 + (size_t)ph * 16);
+    upscale_fwd_kernel<<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h, clamp, pv, tile_c,
+                                                    span_c, span_r); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }

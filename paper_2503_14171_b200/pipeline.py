@@ -20,7 +20,7 @@ import torch
 from . import _lib
 from .device import to_device
 from .raster_forward import Frame, GradientImage, make_view
-from .spline import output_size
+from .spline import output_size, upscale_plan
 
 STAGES = ("prepare", "bin", "raster", "upscale")
 
@@ -55,6 +55,7 @@ class ViewPipeline:
                             else torch.cuda.current_stream(self.scene.device)) for _ in range(slots)]
         self.copy_stream = None
         self.stage_events = None
+        self.plan = upscale_plan(self.width, self.height, self.out_w, self.out_h, self.scene.device)
 
     # ---- capacity -------------------------------------------------------------------------
     def calibrate(self, views, margin: float = 1.05) -> int:
@@ -115,7 +116,8 @@ class ViewPipeline:
             if ev is not None:
                 marks[3].record(slot.stream)
             _lib.check(lib.splat_upscale_forward(_lib.ptr(slot.img.planes), self.width, self.height,
-                                                 _lib.ptr(out), self.out_w, self.out_h, 1, st))
+                                                 _lib.ptr(out), self.out_w, self.out_h, 1,
+                                                 _lib.ptr(self.plan), st))
             if ev is not None:
                 marks[4].record(slot.stream)
                 ev.append(marks)

@@ -21,7 +21,7 @@ from .core import DimensionError, UnsupportedScaleError
 from .raster_forward import GradientImage
 
 __all__ = ["upscale_spline", "upscale_backward", "SourceAdjoint", "fd_gradients",
-           "fd_gradients_backward", "output_size"]
+           "fd_gradients_backward", "output_size", "upscale_plan"]
 
 
 def output_size(in_w: int, in_h: int, factor: float):
@@ -44,6 +44,22 @@ def _planes(img: GradientImage) -> torch.Tensor:
     return p
 
 
+_plans: dict = {}
+
+
+def upscale_plan(in_w: int, in_h: int, out_w: int, out_h: int, device) -> torch.Tensor:
+    """Cached per-size axis maps (splat_upscale_plan)."""
+    key = (in_w, in_h, out_w, out_h, str(device))
+    plan = _plans.get(key)
+    if plan is None:
+        lib = _lib.load()
+        nbytes = lib.splat_upscale_plan_bytes(in_w, in_h, out_w, out_h)
+        plan = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _lib.check(lib.splat_upscale_plan(in_w, in_h, out_w, out_h, _lib.ptr(plan), _lib.stream_ptr()))
+        _plans[key] = plan
+    return plan
+
+
 def upscale_spline(img, factor: float, *, out_size=None, clamp: bool = True,
                    out: torch.Tensor | None = None) -> torch.Tensor:
     """Upscale from value + analytic derivative planes (spline.py:162-178)."""
@@ -58,8 +74,9 @@ def upscale_spline(img, factor: float, *, out_size=None, clamp: bool = True,
     src = _planes(g)
     if out is None:
         out = torch.empty((out_h, out_w, 3), dtype=torch.float32, device=src.device)
+    plan = upscale_plan(g.width, g.height, out_w, out_h, src.device)
     _lib.check(lib.splat_upscale_forward(_lib.ptr(src), g.width, g.height, _lib.ptr(out), out_w, out_h,
-                                         int(bool(clamp)), _lib.stream_ptr()))
+                                         int(bool(clamp)), _lib.ptr(plan), _lib.stream_ptr()))
     return out
 
 
