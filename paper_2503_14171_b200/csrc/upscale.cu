@@ -261,106 +261,165 @@ __device__ __forceinline__ float fma_sat(float a, float b, float c) {
     return r;
 }
 
-__host__ __device__ constexpr int int_tile_cols(int F) { return 64 * F; }
+__host__ __device__ constexpr int int_tile_cols(int F) { return 32 * F; }
 
-template <int F>
+// Hermite weights of phase j for integer factor F: t_j = (j + .5) / F (the
+// fractional position of output pixel F m + F/2 + j inside cell m).  The values
+// are dyadic rationals, exact in float32, and become FFMA immediates.
+__host__ __device__ constexpr float hermite_w(int F, int j, int k) {
+    const double t = (j + 0.5) / F, t2 = t * t, t3 = t2 * t;
+    return (float)(k == 0 ? 1.0 - 3.0 * t2 + 2.0 * t3
+                          : k == 1 ? 3.0 * t2 - 2.0 * t3 : k == 2 ? t - 2.0 * t2 + t3 : t3 - t2);
+}
+
+template <int F, bool CLAMP>
 __global__ void __launch_bounds__(256) upscale_int_kernel(const float* __restrict__ src, int in_w, int in_h,
                                                           float* __restrict__ out, int out_w, int out_h,
-                                                          int clamp, float4 hw0, float4 hw1, float4 hw2,
-                                                          float4 hw3, int span_c, int span_r) {
+                                                          int span_c, int span_r) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ __align__(8) uint64_t s_bar[2];
     constexpr int TC = int_tile_cols(F);
+    constexpr int GPR = TC / 4;            // 4-pixel groups per output row
+    constexpr int NREC = 4 / F + 2;        // G records a group touches
+    constexpr int GCOLS = TC / F + 2;      // G columns (cells) of a tile
+    constexpr int CROWS = kUpRows / F + 1; // cell rows overlapping a tile's rows
     const int tid = threadIdx.x;
-    const int U0 = blockIdx.x * TC, V0 = blockIdx.y * kUpRows;
-    // source columns m(U0) - 1 .. m(U0 + TC - 1) + 1 where cell m = floor((u + .5)/F - .5)
-    const int cx0 = U0 / F - 1, cy0 = V0 / F - 1;
-    const int x0 = max(cx0, 0), x1 = min((U0 + TC) / F, in_w - 1);
-    const int y0 = max(cy0, 0), y1 = min((V0 + kUpRows) / F, in_h - 1);
-    const int ncols = x1 - x0 + 1, nrows = y1 - y0 + 1;
-    float* s_src = reinterpret_cast<float*>(smem);
-    float* s_g = s_src + (size_t)span_r * span_c * 12;
+    const int ntx = (out_w + TC - 1) / TC, nty = (out_h + kUpRows - 1) / kUpRows, ntiles = ntx * nty;
+    const size_t src_floats = (size_t)span_r * span_c * 12;
+    float* const s_src0 = reinterpret_cast<float*>(smem);
+    float* const s_g = s_src0 + 2 * src_floats;
+    float4* const s_xpose = reinterpret_cast<float4*>(s_g + (size_t)kUpRows * GCOLS * 6);  // 8 warps x 96
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[0])));
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    // source box of a tile: cells U0/F - 1 .. (U0 + TC)/F (clamped), rows likewise
+    auto box = [&](int t, int& x0, int& ncols, int& y0, int& nrows) {
+        const int U0 = (t % ntx) * TC, V0 = (t / ntx) * kUpRows;
+        x0 = max(U0 / F - 1, 0);
+        ncols = min((U0 + TC) / F, in_w - 1) - x0 + 1;
+        y0 = max(V0 / F - 1, 0);
+        nrows = min((V0 + kUpRows) / F, in_h - 1) - y0 + 1;
+    };
+    auto issue = [&](int t, int b) {
+        int x0, ncols, y0, nrows;
+        box(t, x0, ncols, y0, nrows);
         const uint32_t row_bytes = (uint32_t)ncols * 48u;
-        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar[b])),
                      "r"(row_bytes * (uint32_t)nrows)
                      : "memory");
+        float* dst = s_src0 + (size_t)b * src_floats;
         for (int r = 0; r < nrows; ++r)
-            bulk_copy(s_src + (size_t)r * span_c * 12, src + ((size_t)(y0 + r) * in_w + x0) * 12, row_bytes,
-                      &s_bar);
-    }
-    __syncthreads();
-    mbar_wait(&s_bar, 0);
-    // Hermite weights of phase j (F <= 4), selected without local memory
-    auto phase_w = [&](int j) { return j == 0 ? hw0 : (j == 1 ? hw1 : (j == 2 ? hw2 : hw3)); };
-    // y pass over the tile rows
-    const int nv = min(kUpRows, out_h - V0);
-    // G columns are indexed by cell column relative to cx0 (clamped reads keep edges right)
-    const int gcols = TC / F + 2;
-    for (int e = tid; e < nv * gcols; e += blockDim.x) {
-        const int v = e / gcols, gc = e - v * gcols;
-        const int vv = V0 + v;
-        const int jy = (vv + F / 2) % F;                 // phase of this output row
-        const int iy = (vv + F / 2) / F - 1;             // floor((v + .5)/F - .5)
-        const float4 h = phase_w(jy);
-        const int ra = clampi(iy, 0, in_h - 1) - y0, rb = clampi(iy + 1, 0, in_h - 1) - y0;
-        const int xc = clampi(cx0 + gc, 0, in_w - 1) - x0;
-        const float4* pa = reinterpret_cast<const float4*>(s_src + ((size_t)ra * span_c + xc) * 12);
-        const float4* pb = reinterpret_cast<const float4*>(s_src + ((size_t)rb * span_c + xc) * 12);
-        const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];
-        const float4 b0 = pb[0], b1 = pb[1], b2 = pb[2];
-        const float fa[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
-        const float fb[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
-        float g[6];
+            bulk_copy(dst + (size_t)r * span_c * 12, src + ((size_t)(y0 + r) * in_w + x0) * 12, row_bytes,
+                      &s_bar[b]);
+    };
+
+    int t = blockIdx.x;
+    if (t < ntiles && tid == 0) issue(t, 0);
+    uint32_t phases = 0u;
+    for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
+        // prefetch the next tile into the other stage while this one is computed
+        if (t + (int)gridDim.x < ntiles && tid == 0) issue(t + gridDim.x, b ^ 1);
+        mbar_wait(&s_bar[b], (phases >> b) & 1u);
+        phases ^= 1u << b;
+        const int U0 = (t % ntx) * TC, V0 = (t / ntx) * kUpRows;
+        const int cx0 = U0 / F - 1, cy0 = V0 / F - 1;
+        int x0, ncols, y0, nrows;
+        box(t, x0, ncols, y0, nrows);
+        const float* sb = s_src0 + (size_t)b * src_floats;
+        const int nv = min(kUpRows, out_h - V0);
+        // y pass, one item per (cell row, cell column): the cell's two corner rows are
+        // read once (6 x LDS.128) and give the G records of its F output rows
+        // G[v][gc] = (value-in-x, slope-in-x) at corner column cx0 + gc.
+        for (int it = tid; it < CROWS * GCOLS; it += blockDim.x) {
+            const int cr = it / GCOLS, gc = it - cr * GCOLS;
+            const int n = cy0 + cr;
+            const int ra = clampi(n, 0, in_h - 1) - y0, rb = clampi(n + 1, 0, in_h - 1) - y0;
+            const int xc = clampi(cx0 + gc, 0, in_w - 1) - x0;
+            const float4* pa = reinterpret_cast<const float4*>(sb + ((size_t)ra * span_c + xc) * 12);
+            const float4* pb = reinterpret_cast<const float4*>(sb + ((size_t)rb * span_c + xc) * 12);
+            const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];
+            const float4 b0 = pb[0], b1 = pb[1], b2 = pb[2];
+            // record = [f0 f1 f2 fx0 | fx1 fx2 fy0 fy1 | fy2 fxy0 fxy1 fxy2]
+            const float fa[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+            const float fb[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            g[c] = fmaf(h.x, fa[c], fmaf(h.y, fb[c], fmaf(h.z, fa[6 + c], h.w * fb[6 + c])));
-            g[3 + c] = fmaf(h.x, fa[3 + c], fmaf(h.y, fb[3 + c], fmaf(h.z, fa[9 + c], h.w * fb[9 + c])));
-        }
-        float2* gd = reinterpret_cast<float2*>(s_g + ((size_t)v * gcols + gc) * 6);
-        gd[0] = make_float2(g[0], g[1]);
-        gd[1] = make_float2(g[2], g[3]);
-        gd[2] = make_float2(g[4], g[5]);
-    }
-    __syncthreads();
-    // x pass: thread -> 4 consecutive pixels u = U0 + 4k .. +3 of row v
-    constexpr int GPR = TC / 4;  // groups per row
-    const int nu = min(TC, out_w - U0);
-    for (int e = tid; e < nv * GPR; e += blockDim.x) {
-        const int v = e / GPR, ug = (e - v * GPR) * 4;
-        if (ug >= nu) continue;
-        float o[12];
+            for (int j = 0; j < F; ++j) {
+                const int v = F * n + F / 2 + j - V0;   // output row of phase j in cell row n
+                if (v < 0 || v >= nv) continue;
+                const float h0 = hermite_w(F, j, 0), h1 = hermite_w(F, j, 1);
+                const float h2 = hermite_w(F, j, 2), h3 = hermite_w(F, j, 3);
+                float g[6];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            // U0 + ug is a multiple of 4 (hence of F): the phase is static per i
-            const int jx = (i + F / 2) % F;
-            const int ix = (U0 + ug) / F + (i + F / 2) / F - 1;   // cell column of this pixel
-            const float4 h = jx == 0 ? hw0 : (jx == 1 ? hw1 : (jx == 2 ? hw2 : hw3));
-            const int gca = ix - cx0, gcb = gca + 1;      // G columns of the two corners
-            const float2* ga = reinterpret_cast<const float2*>(s_g + ((size_t)v * gcols + gca) * 6);
-            const float2* gb = reinterpret_cast<const float2*>(s_g + ((size_t)v * gcols + gcb) * 6);
-            const float2 a0 = ga[0], a1 = ga[1], a2 = ga[2], b0 = gb[0], b1 = gb[1], b2 = gb[2];
-            const float A[6] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y};
-            const float B[6] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y};
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const float part = fmaf(h.y, B[c], fmaf(h.z, A[3 + c], h.w * B[3 + c]));
-                o[3 * i + c] = clamp ? fma_sat(h.x, A[c], part) : fmaf(h.x, A[c], part);
+                for (int c = 0; c < 3; ++c) {
+                    g[c] = fmaf(h0, fa[c], fmaf(h1, fb[c], fmaf(h2, fa[6 + c], h3 * fb[6 + c])));
+                    g[3 + c] = fmaf(h0, fa[3 + c], fmaf(h1, fb[3 + c], fmaf(h2, fa[9 + c], h3 * fb[9 + c])));
+                }
+                float2* gd = reinterpret_cast<float2*>(s_g + ((size_t)v * GCOLS + gc) * 6);
+                gd[0] = make_float2(g[0], g[1]);
+                gd[1] = make_float2(g[2], g[3]);
+                gd[2] = make_float2(g[4], g[5]);
             }
         }
-        float* dst = out + ((size_t)(V0 + v) * out_w + U0 + ug) * 3;
-        if (ug + 3 < nu && (out_w & 3) == 0) {
-            float4* d4 = reinterpret_cast<float4*>(dst);
-            __stcs(d4, make_float4(o[0], o[1], o[2], o[3]));
-            __stcs(d4 + 1, make_float4(o[4], o[5], o[6], o[7]));
-            __stcs(d4 + 2, make_float4(o[8], o[9], o[10], o[11]));
-        } else {
-            for (int i = 0; i < 4 && ug + i < nu; ++i)
-                for (int c = 0; c < 3; ++c) dst[3 * i + c] = o[3 * i + c];
+        __syncthreads();
+        // x pass: thread -> 4 consecutive pixels u = U0 + ug .. +3 of row v, whose corner
+        // columns are the cells base-1 .. base+4/F (NREC G records, each loaded once)
+        const int nu = min(TC, out_w - U0);
+        for (int e = tid; e < nv * GPR; e += blockDim.x) {
+            const int v = e / GPR, ug = (e - v * GPR) * 4;
+            if (ug >= nu) continue;
+            const int r0 = (U0 + ug) / F - 1 - cx0;   // G column of record 0
+            const float2* gp = reinterpret_cast<const float2*>(s_g + ((size_t)v * GCOLS + r0) * 6);
+            float R[NREC][6];
+#pragma unroll
+            for (int k = 0; k < NREC; ++k) {
+                const float2 q0 = gp[3 * k], q1 = gp[3 * k + 1], q2 = gp[3 * k + 2];
+                R[k][0] = q0.x;
+                R[k][1] = q0.y;
+                R[k][2] = q1.x;
+                R[k][3] = q1.y;
+                R[k][4] = q2.x;
+                R[k][5] = q2.y;
+            }
+            float o[12];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                // pixel U0 + ug + i (U0 + ug is a multiple of F): phase and left record are static
+                const int jx = (i + F / 2) % F;
+                const int ka = (i + F / 2) / F;
+                const float h0 = hermite_w(F, jx, 0), h1 = hermite_w(F, jx, 1);
+                const float h2 = hermite_w(F, jx, 2), h3 = hermite_w(F, jx, 3);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const float part = fmaf(h1, R[ka + 1][c], fmaf(h2, R[ka][3 + c], h3 * R[ka + 1][3 + c]));
+                    o[3 * i + c] = CLAMP ? fma_sat(h0, R[ka][c], part) : fmaf(h0, R[ka][c], part);
+                }
+            }
+            // the lanes of one row segment (GPR = 32 or 16 groups) transpose their
+            // 48-byte outputs through shared memory so every 16-byte store
+            // instruction writes whole 128-byte lines (512 or 2 x 256 contiguous bytes)
+            if ((out_w & 3) == 0 && nu == TC) {
+                const int lane = tid & 31, li = lane % GPR;
+                float4* w4 = s_xpose + (tid >> 5) * 96 + (lane / GPR) * 3 * GPR;
+                w4[3 * li] = make_float4(o[0], o[1], o[2], o[3]);
+                w4[3 * li + 1] = make_float4(o[4], o[5], o[6], o[7]);
+                w4[3 * li + 2] = make_float4(o[8], o[9], o[10], o[11]);
+                __syncwarp();
+                float4* d4 = reinterpret_cast<float4*>(out + ((size_t)(V0 + v) * out_w + U0) * 3);
+                __stcs(d4 + li, w4[li]);
+                __stcs(d4 + GPR + li, w4[GPR + li]);
+                __stcs(d4 + 2 * GPR + li, w4[2 * GPR + li]);
+                __syncwarp();
+            } else {
+                float* dst = out + ((size_t)(V0 + v) * out_w + U0 + ug) * 3;
+                for (int i = 0; i < 4 && ug + i < nu; ++i)
+                    for (int c = 0; c < 3; ++c) dst[3 * i + c] = o[3 * i + c];
+            }
         }
+        __syncthreads();
     }
 }
 
@@ -583,35 +642,27 @@ int upscale_plan_impl(int in_w, int in_h, int out_w, int out_h, void* plan, cuda
     return SPLAT_OK;
 }
 
-template <int F>
-static int upscale_int_launch(const float* src, int in_w, int in_h, float* out, int out_w, int out_h, int clamp,
+template <int F, bool CLAMP>
+static int upscale_int_launch(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
                               cudaStream_t stream) {
     constexpr int TC = int_tile_cols(F);
     const int span_c = TC / F + 3, span_r = kUpRows / F + 3;
-    const size_t smem = (size_t)span_r * span_c * 48 + (size_t)kUpRows * (TC / F + 2) * 24;
-    static int configured = 0;
-    if (!configured) {
-        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_int_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)smem));
-        configured = 1;
+    const size_t smem = 2 * (size_t)span_r * span_c * 48 + (size_t)kUpRows * (TC / F + 2) * 24 + 8 * 96 * 16;
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_int_kernel<F, CLAMP>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SPLAT_CUDA_CHECK(
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_int_kernel<F, CLAMP>, 256, smem));
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (per_sm < 1) per_sm = 1;
     }
-    // Hermite weights of the F phases: t_j = (j + .5) / F - .5 + (j < F/2 ? 1 : 0)
-    float4 hw[4];
-    for (int j = 0; j < 4; ++j) {
-        double t = j < F ? ((double)j + 0.5) / F - 0.5 + (j < F / 2 ? 1.0 : 0.0) : 0.0;
-        // phase j is defined by (u + F/2) % F; recover t from s = (u+.5)/F - .5
-        if (j < F) {
-            int u = (j - F / 2 + F) % F + F;  // any u with that phase (>= 0)
-            double s = ((double)u + 0.5) / F - 0.5;
-            t = s - floor(s);
-        }
-        double t2 = t * t, t3 = t2 * t;
-        hw[j] = make_float4((float)(1.0 - 3.0 * t2 + 2.0 * t3), (float)(3.0 * t2 - 2.0 * t3),
-                            (float)(t - 2.0 * t2 + t3), (float)(t3 - t2));
-    }
-    dim3 grid(ceil_div(out_w, TC), ceil_div(out_h, kUpRows));
-    upscale_int_kernel<F><<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h, clamp, hw[0], hw[1],
-                                                       hw[2], hw[3], span_c, span_r); note_launch();
+    const int ntiles = ceil_div(out_w, TC) * ceil_div(out_h, kUpRows);
+    const int grid = max(1, min(ntiles, per_sm * sms));
+    upscale_int_kernel<F, CLAMP><<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h, span_c,
+                                                              span_r); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
@@ -620,9 +671,11 @@ int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int o
                          int clamp, const void* plan, cudaStream_t stream) {
     if (out_w <= 0 || out_h <= 0) return SPLAT_OK;
     if (out_w == 4 * in_w && out_h == 4 * in_h)
-        return upscale_int_launch<4>(src, in_w, in_h, out, out_w, out_h, clamp, stream);
+        return clamp ? upscale_int_launch<4, true>(src, in_w, in_h, out, out_w, out_h, stream)
+                     : upscale_int_launch<4, false>(src, in_w, in_h, out, out_w, out_h, stream);
     if (out_w == 2 * in_w && out_h == 2 * in_h)
-        return upscale_int_launch<2>(src, in_w, in_h, out, out_w, out_h, clamp, stream);
+        return clamp ? upscale_int_launch<2, true>(src, in_w, in_h, out, out_w, out_h, stream)
+                     : upscale_int_launch<2, false>(src, in_w, in_h, out, out_w, out_h, stream);
     double sx = (double)out_w / (double)in_w, sy = (double)out_h / (double)in_h;
     int tile_c = sx >= 4.0 ? 256 : (sx >= 2.0 ? 128 : 64);
     int span_c = (int)ceil((tile_c - 1) / sx) + 3;
