@@ -423,6 +423,139 @@ __global__ void __launch_bounds__(256) upscale_int_kernel(const float* __restric
     }
 }
 
+// x4 fast path (the headline configuration).  One thread owns one cell row n
+// and one 4-pixel column group g: output rows 4n+2 .. 4n+5 (phases 0..3 of
+// the cell) x pixels 4g .. 4g+3 (phases 2,3 of cell g-1 and 0,1 of cell g).
+// It reads its 6 corner records (corner columns g-1..g+1, rows n, n+1) from
+// the TMA-staged source tile once, runs y pass + x pass in registers (no
+// shared-memory intermediate, no barrier between the passes) and writes
+// 4 rows x 48 bytes with 16-byte streaming stores.  A CTA = 8 warps = 8 cell
+// rows x 32 groups (32 x 128 output pixels); persistent, double-buffered.
+constexpr int kX4Groups = 32;                // groups (4 px) per tile row = one warp
+constexpr int kX4CellRows = 8;               // cell rows per tile = warps per CTA
+constexpr int kX4SpanC = kX4Groups + 2;      // corner columns of a tile
+constexpr int kX4SpanR = kX4CellRows + 1;    // corner rows of a tile
+
+template <bool CLAMP>
+__global__ void __launch_bounds__(256) upscale_x4_kernel(const float* __restrict__ src, int in_w, int in_h,
+                                                         float* __restrict__ out, int out_w, int out_h) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    constexpr size_t kStage = (size_t)kX4SpanR * kX4SpanC * 12;   // floats per stage
+    float* const s_src0 = reinterpret_cast<float*>(smem);
+    float4* const s_xp = reinterpret_cast<float4*>(s_src0 + 2 * kStage);  // 8 warps x 96 float4
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ngx = (out_w / 4 + kX4Groups - 1) / kX4Groups;     // tiles along x
+    const int ngy = (in_h + 1 + kX4CellRows - 1) / kX4CellRows;  // cell rows -1 .. in_h-1
+    const int ntiles = ngx * ngy;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[0])));
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    // tile t: groups g0 .. g0+31, cell rows n0 .. n0+7 (n0 = 8 ty - 1); its corner box is
+    // columns g0-1 .. g0+32 and rows n0 .. n0+8, clamped to the image (edge replication)
+    auto box = [&](int t, int& x0, int& ncols, int& y0, int& nrows) {
+        const int g0 = (t % ngx) * kX4Groups, n0 = (t / ngx) * kX4CellRows - 1;
+        x0 = max(g0 - 1, 0);
+        ncols = min(g0 + kX4Groups, in_w - 1) - x0 + 1;
+        y0 = max(n0, 0);
+        nrows = min(n0 + kX4CellRows, in_h - 1) - y0 + 1;
+    };
+    auto issue = [&](int t, int b) {
+        int x0, ncols, y0, nrows;
+        box(t, x0, ncols, y0, nrows);
+        const uint32_t row_bytes = (uint32_t)ncols * 48u;
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar[b])),
+                     "r"(row_bytes * (uint32_t)nrows)
+                     : "memory");
+        float* dst = s_src0 + (size_t)b * kStage;
+        for (int r = 0; r < nrows; ++r)
+            bulk_copy(dst + (size_t)r * kX4SpanC * 12, src + ((size_t)(y0 + r) * in_w + x0) * 12, row_bytes,
+                      &s_bar[b]);
+    };
+
+    int t = blockIdx.x;
+    if (t < ntiles && tid == 0) issue(t, 0);
+    uint32_t phases = 0u;
+    for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
+        if (t + (int)gridDim.x < ntiles && tid == 0) issue(t + gridDim.x, b ^ 1);
+        mbar_wait(&s_bar[b], (phases >> b) & 1u);
+        phases ^= 1u << b;
+        int x0, ncols, y0, nrows;
+        box(t, x0, ncols, y0, nrows);
+        const int g = (t % ngx) * kX4Groups + lane;
+        const int n = (t / ngx) * kX4CellRows - 1 + warp;
+        const unsigned active = __ballot_sync(0xffffffffu, g < out_w / 4);
+        if (g < out_w / 4 && n < in_h) {
+            const float* sb = s_src0 + (size_t)b * kStage;
+            // corner records: columns g-1, g, g+1; rows n, n+1 (edge-clamped)
+            float rec[2][3][12];
+#pragma unroll
+            for (int ry = 0; ry < 2; ++ry) {
+                const int row = clampi(n + ry, 0, in_h - 1) - y0;
+#pragma unroll
+                for (int cx = 0; cx < 3; ++cx) {
+                    const int col = clampi(g - 1 + cx, 0, in_w - 1) - x0;
+                    const float4* p = reinterpret_cast<const float4*>(sb + ((size_t)row * kX4SpanC + col) * 12);
+                    const float4 q0 = p[0], q1 = p[1], q2 = p[2];
+                    float* r = rec[ry][cx];
+                    r[0] = q0.x; r[1] = q0.y; r[2] = q0.z; r[3] = q0.w;
+                    r[4] = q1.x; r[5] = q1.y; r[6] = q1.z; r[7] = q1.w;
+                    r[8] = q2.x; r[9] = q2.y; r[10] = q2.z; r[11] = q2.w;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {              // output row 4n + 2 + j
+                const int v = 4 * n + 2 + j;
+                if (v < 0 || v >= out_h) continue;
+                const float h0 = hermite_w(4, j, 0), h1 = hermite_w(4, j, 1);
+                const float h2 = hermite_w(4, j, 2), h3 = hermite_w(4, j, 3);
+                // y pass: value-in-x (f, fy) and slope-in-x (fx, fxy) per corner column
+                float G[3][6];
+#pragma unroll
+                for (int cx = 0; cx < 3; ++cx)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float* a = rec[0][cx];
+                        const float* bb = rec[1][cx];
+                        G[cx][c] = fmaf(h0, a[c], fmaf(h1, bb[c], fmaf(h2, a[6 + c], h3 * bb[6 + c])));
+                        G[cx][3 + c] = fmaf(h0, a[3 + c], fmaf(h1, bb[3 + c], fmaf(h2, a[9 + c], h3 * bb[9 + c])));
+                    }
+                // x pass: pixel i has phase (i + 2) % 4 in cell g - 1 + (i >= 2)
+                float o[12];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int jx = (i + 2) % 4, ka = (i + 2) / 4;
+                    const float w0 = hermite_w(4, jx, 0), w1 = hermite_w(4, jx, 1);
+                    const float w2 = hermite_w(4, jx, 2), w3 = hermite_w(4, jx, 3);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float part = fmaf(w1, G[ka + 1][c], fmaf(w2, G[ka][3 + c], w3 * G[ka + 1][3 + c]));
+                        o[3 * i + c] = CLAMP ? fma_sat(w0, G[ka][c], part) : fmaf(w0, G[ka][c], part);
+                    }
+                }
+                // transpose the warp's 128 pixels (1536 B) through shared memory so each
+                // 16-byte store instruction writes 512 contiguous bytes (whole lines)
+                float4* w4 = s_xp + warp * 96;
+                w4[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
+                w4[3 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
+                w4[3 * lane + 2] = make_float4(o[8], o[9], o[10], o[11]);
+                __syncwarp(active);
+                const int gw = (t % ngx) * kX4Groups;        // first group of this warp row
+                float4* d4 = reinterpret_cast<float4*>(out + ((size_t)v * out_w + 4 * gw) * 3);
+                const int nvalid = 3 * min(kX4Groups, out_w / 4 - gw);
+                const int nact = __popc(active);   // active lanes are 0 .. nact-1
+                for (int k = lane; k < nvalid; k += nact) __stcs(d4 + k, w4[k]);
+                __syncwarp(active);
+            }
+        }
+        __syncthreads();   // stage b is refilled by the prefetch of the next iteration
+    }
+}
+
 // ---- backward -----------------------------------------------------------------
 
 constexpr int kBwRows = 16;
@@ -667,12 +800,34 @@ static int upscale_int_launch(const float* src, int in_w, int in_h, float* out, 
     return SPLAT_OK;
 }
 
+template <bool CLAMP>
+static int upscale_x4_launch(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
+                             cudaStream_t stream) {
+    const size_t smem = 2 * (size_t)kX4SpanR * kX4SpanC * 48 + 8 * 96 * 16;
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_x4_kernel<CLAMP>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SPLAT_CUDA_CHECK(
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_x4_kernel<CLAMP>, 256, smem));
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int ntiles = ceil_div(out_w / 4, kX4Groups) * ceil_div(in_h + 1, kX4CellRows);
+    const int grid = max(1, min(ntiles, per_sm * sms));
+    upscale_x4_kernel<CLAMP><<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h); note_launch();
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
+
 int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
                          int clamp, const void* plan, cudaStream_t stream) {
     if (out_w <= 0 || out_h <= 0) return SPLAT_OK;
     if (out_w == 4 * in_w && out_h == 4 * in_h)
-        return clamp ? upscale_int_launch<4, true>(src, in_w, in_h, out, out_w, out_h, stream)
-                     : upscale_int_launch<4, false>(src, in_w, in_h, out, out_w, out_h, stream);
+        return clamp ? upscale_x4_launch<true>(src, in_w, in_h, out, out_w, out_h, stream)
+                     : upscale_x4_launch<false>(src, in_w, in_h, out, out_w, out_h, stream);
     if (out_w == 2 * in_w && out_h == 2 * in_h)
         return clamp ? upscale_int_launch<2, true>(src, in_w, in_h, out, out_w, out_h, stream)
                      : upscale_int_launch<2, false>(src, in_w, in_h, out, out_w, out_h, stream);
