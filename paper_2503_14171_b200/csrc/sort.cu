@@ -128,54 +128,107 @@ radix_upsweep_kernel(const K* __restrict__ keys, const uint32_t* n_dev, int64_t 
     hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
 }
 
+// Downsweep: warp w of the CTA owns the contiguous sub-chunk
+// [base + w*32*R, base + (w+1)*32*R) and keeps its R items per lane in
+// registers.  Pass 1 counts digits per warp (one __match_any_sync per item,
+// the group leader accumulates into the warp's 256 counters).  The CTA then
+// derives each item's position in the block-locally sorted order (digit-major,
+// stable) and its digit's global base.  Pass 2 writes items to shared memory at
+// their local position; finally the CTA streams shared memory out, so each
+// digit run is written to global memory with consecutive (coalesced) stores.
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
 radix_downsweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                        K* __restrict__ kout, uint32_t* __restrict__ vout,
                        const uint32_t* n_dev, int64_t n_host, int64_t cap, int shift,
                        const uint32_t* __restrict__ hist, int nblocks) {
-    __shared__ uint32_t s_run[256];
-    __shared__ uint32_t s_wcnt[8][256];
+    constexpr int R = kSortRounds;
+    extern __shared__ __align__(16) unsigned char sm[];
+    uint32_t(*s_cnt)[256] = reinterpret_cast<uint32_t(*)[256]>(sm);            // [8][256]
+    uint32_t* s_gbase = reinterpret_cast<uint32_t*>(sm + 8 * 256 * 4);           // [256]
+    uint32_t* s_scan = s_gbase + 256;                                          // [33]
+    K* s_k = reinterpret_cast<K*>(sm + 8 * 256 * 4 + 512 * 4);                 // [kSortTile]
+    uint32_t* s_v = reinterpret_cast<uint32_t*>(s_k + kSortTile);              // [kSortTile]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t n = sort_count(n_dev, n_host, cap);
-    int64_t base = (int64_t)blockIdx.x * kSortTile;
+    const uint32_t n = sort_count(n_dev, n_host, cap);
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
     if (base >= n) return;
-    s_run[tid] = hist[(int64_t)tid * nblocks + blockIdx.x];
+    const int nblk = (int)min((int64_t)kSortTile, (int64_t)n - base);
+    const int64_t sub = base + (int64_t)warp * 32 * R;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int r = 0; r < kSortRounds; ++r) {
-        int64_t i = base + r * kSortThreads + tid;
-        if (base + r * kSortThreads >= n) break;  // uniform across the block
+    K k[R];
+    uint32_t v[R], peers[R];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) s_wcnt[w][tid] = 0;
-        __syncthreads();
-        bool valid = i < n;
-        K k = valid ? kin[i] : K(0);
-        uint32_t v = valid ? vin[i] : 0u;
-        uint32_t d = (uint32_t)(k >> shift) & 0xffu;
-        uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-        uint32_t rank_in_warp = 0;
-        if (valid) {
-            uint32_t peers = __match_any_sync(vmask, d);
-            rank_in_warp = __popc(peers & lt_mask);
-            if (rank_in_warp == 0) s_wcnt[warp][d] = __popc(peers);
-        }
-        __syncthreads();
-        uint32_t run = s_run[tid];
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            uint32_t c = s_wcnt[w][tid];
-            s_wcnt[w][tid] = run;
-            run += c;
-        }
-        s_run[tid] = run;
-        __syncthreads();
-        if (valid) {
-            uint32_t pos = s_wcnt[warp][d] + rank_in_warp;
-            kout[pos] = k;
-            vout[pos] = v;
-        }
-        __syncthreads();
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = sub + r * 32 + lane;
+        const bool valid = i < n;
+        k[r] = valid ? kin[i] : K(0);
+        v[r] = valid ? vin[i] : 0u;
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s_cnt[warp][lane + 32 * q] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const bool valid = sub + r * 32 + lane < n;
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+        const uint32_t d = (uint32_t)(k[r] >> shift) & 0xffu;
+        peers[r] = 0;
+        if (valid) {
+            peers[r] = __match_any_sync(vmask, d);
+            if ((peers[r] & lt_mask) == 0) s_cnt[warp][d] += __popc(peers[r]);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // thread t = digit t: warp prefix, block total, block-local digit offset
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const uint32_t c = s_cnt[w][tid];
+        s_cnt[w][tid] = tot;
+        tot += c;
+    }
+    uint32_t incl = tot;   // inclusive scan of tot over the 256 digits (8 warps x 32)
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, dd);
+        if (lane >= dd) incl += o;
+    }
+    if (lane == 31) s_scan[warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_scan[w];
+    const uint32_t loff = wpre + incl - tot;   // exclusive
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s_cnt[w][tid] += loff;
+    s_gbase[tid] = hist[(int64_t)tid * nblocks + blockIdx.x] - loff;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t d = (uint32_t)(k[r] >> shift) & 0xffu;
+        uint32_t pos = 0;
+        if (peers[r]) pos = s_cnt[warp][d] + __popc(peers[r] & lt_mask);
+        __syncwarp();
+        if (peers[r]) {
+            if ((peers[r] & lt_mask) == 0) s_cnt[warp][d] += __popc(peers[r]);
+            s_k[pos] = k[r];
+            s_v[pos] = v[r];
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int i = tid; i < nblk; i += kSortThreads) {
+        const K kk = s_k[i];
+        const uint32_t pos = s_gbase[(uint32_t)(kk >> shift) & 0xffu] + (uint32_t)i;
+        kout[pos] = kk;
+        vout[pos] = s_v[i];
+    }
+}
+
+template <typename K>
+constexpr size_t downsweep_smem() {
+    return 8 * 256 * 4 + 512 * 4 + (size_t)kSortTile * (sizeof(K) + 4);
 }
 
 }  // namespace
@@ -209,6 +262,13 @@ int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, c
     if (nb == 0) nb = 1;
     uint32_t* hist = scratch;
     uint32_t* hscan = scratch + 256 * (int64_t)nb + 1;
+    static bool configured = false;
+    if (!configured) {
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(radix_downsweep_kernel<K>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)downsweep_smem<K>()));
+        configured = true;
+    }
     K* src_k = keys;
     uint32_t* src_v = vals;
     K* dst_k = keys_alt;
@@ -218,7 +278,7 @@ int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, c
         radix_upsweep_kernel<K><<<nb, kSortThreads, 0, stream>>>(src_k, n_dev, n_host, cap, shift,
                                                                  hist, nb); note_launch();
         exclusive_scan_u32(hist, hist, 256 * (int64_t)nb, hscan, nullptr, stream);
-        radix_downsweep_kernel<K><<<nb, kSortThreads, 0, stream>>>(src_k, src_v, dst_k, dst_v,
+        radix_downsweep_kernel<K><<<nb, kSortThreads, downsweep_smem<K>(), stream>>>(src_k, src_v, dst_k, dst_v,
                                                                    n_dev, n_host, cap, shift, hist, nb); note_launch();
         K* tk = src_k; src_k = dst_k; dst_k = tk;
         uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
