@@ -79,6 +79,20 @@ __device__ __noinline__ int eval_exact(const SceneConst& sc, const ViewConst& vc
     return eval_exact_inl(sc, vc, bboxes, r, px, py, alpha64);
 }
 
+// 2^x via MUFU.EX2 (flush-to-zero: results below 2^-126 are far below the cull).
+// Max relative error 2^-22, inside the 2^-20 budget of eval_fast's `rel`.
+__device__ __forceinline__ float fast_exp2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float fast_rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // Float32 footprint with a certified decision (_kernels.py:65-87).  Returns
 // kCulled / kContrib / kClamped when the float32 evaluation decides the
 // reference's tests with margin, kUnsure otherwise.  `al` etc. are the
@@ -111,8 +125,7 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
         }
         return kUnsure;
     }
-    float e = __expf(-qf);
-    al = g.sigma * e;
+    al = g.sigma * fast_exp2(-1.44269504f * qf);
     float gx = -2.f * fmaf(g.b, dy, adx);
     float gy = -2.f * fmaf(g.b, dx, g.c * dy);
     ax = al * gx;
@@ -134,7 +147,7 @@ __device__ __forceinline__ void canonical_values(const PackF& g, float cx, float
     float adx = g.a * dx;
     float b2 = 2.f * g.b;
     float qf = ((adx * dx) + ((b2 * dx) * dy)) + ((g.c * dy) * dy);
-    al = g.sigma * __expf(-qf);
+    al = g.sigma * fast_exp2(-1.44269504f * qf);
     float gx = -2.f * fmaf(g.b, dy, adx);
     float gy = -2.f * fmaf(g.b, dx, g.c * dy);
     ax = al * gx;
@@ -309,36 +322,45 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
     s.add(al, gax, gay, gaxy, om, col);
     s.last = j + 1;
     // relative error bound of T: error of om plus one rounding of the product
-    s.eps += fmaf(__fdividef(al, om), rel, 1.2e-7f);
-    // T = T_exact (1 +- eps) to first order; 1e-4f and the float compare add < 1e-7
-    const float m = fmaf(1.0625f, s.eps, 2e-7f);
+    s.eps += fmaf(al * fast_rcp(om), rel, 1.2e-7f);
+    // T = T_exact (1 +- eps) to first order; 1e-4f and the float compare add < 1e-7.
+    // eps stays far below 1e-2 (flagged pixels stop), so T > 1.02e-4 is never a decision.
     const float T = s.T;
-    if (T < kTermF * (1.f - m)) {
-        active = false;  // certainly terminated (_kernels.py:110-111)
-    } else if (T <= kTermF * (1.f + m)) {
-        active = false;  // too close to call in float32: exact re-render
-        flagged = true;
+    if (T <= 1.02e-4f) {
+        const float m = fmaf(1.0625f, s.eps, 2e-7f);
+        if (T < kTermF * (1.f - m)) {
+            active = false;  // certainly terminated (_kernels.py:110-111)
+        } else if (T <= kTermF * (1.f + m)) {
+            active = false;  // too close to call in float32: exact re-render
+            flagged = true;
+        }
     }
 }
 
-// Each warp streams the tile's candidate list itself (no block barriers):
-// 32 candidates per step are loaded one per lane, culled against the warp's
-// 8x4 pixel rectangle with the exact ellipse test, compacted into the warp's
-// shared-memory slice, then blended in depth order by every lane (pixel).
+// Each warp streams the tile's candidate list itself (no block barriers).  The
+// warp's 8x4 pixel rectangle is split into four 4x2 groups of 8 lanes; 32
+// candidates per step are loaded one per lane, culled against the warp
+// rectangle and then each group rectangle with the exact ellipse test, staged
+// in the warp's shared-memory slice, and compacted into one in-order list per
+// group.  Step k of the blend loop then advances every group by one of ITS
+// candidates (four candidates per warp instruction stream), which roughly
+// halves the lanes idling on candidates that miss their pixels.
 template <bool TRAIN>
 __global__ void __launch_bounds__(kBlock, 3) raster_fwd_kernel(RasterArgs p) {
     __shared__ PackF s_pack[kWarps][32];
     __shared__ float4 s_col[kWarps][32];
     __shared__ uint2 s_id[kWarps][32];   // (rank, list index)
+    __shared__ uint8_t s_list[kWarps][4][32];
 
     const int tile = blockIdx.x;
     const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = lane >> 3, li = lane & 7;
     const int rx0 = tile_x * kTile + (warp & 1) * 8, ry0 = tile_y * kTile + (warp >> 1) * 4;
-    const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3);
+    const int px = rx0 + (q & 1) * 4 + (li & 3), py = ry0 + (q >> 1) * 2 + (li >> 2);
     const bool inside = px < p.width && py < p.height;
     const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
-    const float X0 = (float)rx0 + 0.5f, X1 = X0 + 7.f, Y0 = (float)ry0 + 0.5f, Y1 = Y0 + 3.f;
+    const float X0 = (float)rx0 + 0.5f, Y0 = (float)ry0 + 0.5f;
     const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
     const uint32_t lt = (1u << lane) - 1u;
 
@@ -351,27 +373,42 @@ __global__ void __launch_bounds__(kBlock, 3) raster_fwd_kernel(RasterArgs p) {
     if (__any_sync(0xffffffffu, active)) {
         for (uint32_t base = start; base < end; base += 32) {
             const uint32_t j = base + lane;
-            bool keep = false;
+            uint32_t gmask = 0;   // bit q: candidate reaches group q's 4x2 rectangle
             PackF g;
             uint32_t r = 0;
             if (j < end) {
                 r = p.ranks[j];
                 g = p.pack[r];
-                keep = ellipse_hits_rect(g, X0, X1, Y0, Y1);
+                if (ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        const float gx0 = X0 + 4.f * (qq & 1), gy0 = Y0 + 2.f * (qq >> 1);
+                        if (ellipse_hits_rect(g, gx0, gx0 + 3.f, gy0, gy0 + 1.f)) gmask |= 1u << qq;
+                    }
+                }
             }
-            const uint32_t m = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                const int pos = __popc(m & lt);
-                s_pack[warp][pos] = g;
-                s_col[warp][pos] = p.sc.color[r];
-                s_id[warp][pos] = make_uint2(r, j);
+            const uint32_t m = __ballot_sync(0xffffffffu, gmask != 0);
+            const int slot = __popc(m & lt);
+            if (gmask) {
+                s_pack[warp][slot] = g;
+                s_col[warp][slot] = p.sc.color[r];
+                s_id[warp][slot] = make_uint2(r, j);
+            }
+            int cnt_my = 0, cnt_max = 0;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const uint32_t mq = __ballot_sync(0xffffffffu, (gmask >> qq) & 1u);
+                if ((gmask >> qq) & 1u) s_list[warp][qq][__popc(mq & lt)] = (uint8_t)slot;
+                const int c = __popc(mq);
+                cnt_max = max(cnt_max, c);
+                if (qq == q) cnt_my = c;
             }
             __syncwarp();
-            const int cnt = __popc(m);
-            for (int k = 0; k < cnt; ++k) {
-                if (active) {
-                    const uint2 id = s_id[warp][k];
-                    blend_candidate<TRAIN>(p, s_pack[warp][k], s_col[warp][k], id.x, id.y, px, py, cx, cy,
+            for (int k = 0; k < cnt_max; ++k) {
+                if (active && k < cnt_my) {
+                    const int idx = s_list[warp][q][k];
+                    const uint2 id = s_id[warp][idx];
+                    blend_candidate<TRAIN>(p, s_pack[warp][idx], s_col[warp][idx], id.x, id.y, px, py, cx, cy,
                                            s, active, flagged);
                 }
                 if ((k & 7) == 7 && !__any_sync(0xffffffffu, active)) break;
