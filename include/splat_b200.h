@@ -80,7 +80,7 @@ typedef struct {
     uint32_t *counters;     /* [0]=pairs [1]=overflow [2]=fix-up pixels; [4]=sticky overflow
                                (never cleared by the library: the caller zeroes it) */
     uint32_t *fixup;        /* (H*W) pixels re-rendered by the exact float64 pass */
-    float *pack;            /* (n,12) float32 per-view pack */
+    float *pack;            /* (n,16) float32 per-view pack */
 } splat_frame_ptrs_t;
 
 const char *splat_last_error(void);

@@ -12,7 +12,8 @@ import os
 from .core import DimensionError, ParameterError, UnsupportedScaleError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsplat_b200.so")
+# SPLAT_B200_LIB selects an alternative in-tree build (kernel tuning experiments)
+LIB_PATH = os.environ.get("SPLAT_B200_LIB", os.path.join(_HERE, "libsplat_b200.so"))
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int

@@ -30,11 +30,12 @@ struct SceneConst {
     const float4* color;    // (n) float32 rgb_ colours in rank order
 };
 
-// Per-view float32 pack the rasterizer consumes (rank order, 48 bytes).
+// Per-view float32 pack the rasterizer consumes (rank order, 64 bytes).
 struct __align__(16) PackF {
     float mxh, mxl, myh, myl;     // render-space mean as float hi + lo parts
     float a, b, c, sigma;         // conic and opacity
     float qcull, qclamp, pad0, pad1;  // ln(255 sigma), ln(sigma / 0.999), b/a, b/c
+    float ex, ey, pad2, pad3;     // half extents of the cull ellipse, padded (pre-filter only)
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

@@ -117,6 +117,12 @@ __global__ void preprocess_kernel(SceneConst sc, ViewConst vc, int width, int he
     p.qclamp = (float)log(sg / kAlphaClamp);
     p.pad0 = (float)(b / a);  // ellipse-rectangle test: edge minimisers (raster_fwd.cu)
     p.pad1 = (float)(b / c);
+    // cull-ellipse half extents (the reference's rx, ry) with a 1e-3 px + 1e-5 relative
+    // margin: every pixel centre that can contribute lies in mean +- (ex, ey)
+    p.ex = (float)(rx * (1.0 + 1e-5) + 1e-3);
+    p.ey = (float)(ry * (1.0 + 1e-5) + 1e-3);
+    p.pad2 = 0.f;
+    p.pad3 = 0.f;
     pack[r] = p;
 }
 

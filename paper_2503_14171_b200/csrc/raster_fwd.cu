@@ -346,7 +346,10 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 // candidates (four candidates per warp instruction stream), which roughly
 // halves the lanes idling on candidates that miss their pixels.
 template <bool TRAIN>
-__global__ void __launch_bounds__(kBlock, 3) raster_fwd_kernel(RasterArgs p) {
+#ifndef RASTER_MIN_BLOCKS
+#define RASTER_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kBlock, RASTER_MIN_BLOCKS) raster_fwd_kernel(RasterArgs p) {
     __shared__ PackF s_pack[kWarps][32];
     __shared__ float4 s_col[kWarps][32];
     __shared__ uint2 s_id[kWarps][32];   // (rank, list index)
@@ -380,11 +383,14 @@ __global__ void __launch_bounds__(kBlock, 3) raster_fwd_kernel(RasterArgs p) {
                 r = p.ranks[j];
                 g = p.pack[r];
                 if (ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
-#pragma unroll
-                    for (int qq = 0; qq < 4; ++qq) {
-                        const float gx0 = X0 + 4.f * (qq & 1), gy0 = Y0 + 2.f * (qq >> 1);
-                        if (ellipse_hits_rect(g, gx0, gx0 + 3.f, gy0, gy0 + 1.f)) gmask |= 1u << qq;
-                    }
+                    // groups: the cull ellipse's extent box against each 4x2 rectangle
+                    const float lx = g.mxh - g.ex, hx = g.mxh + g.ex;
+                    const float ly = g.myh - g.ey, hy = g.myh + g.ey;
+                    const uint32_t c0 = (lx <= X0 + 3.f && hx >= X0) ? 1u : 0u;
+                    const uint32_t c1 = (lx <= X0 + 7.f && hx >= X0 + 4.f) ? 1u : 0u;
+                    const uint32_t r0 = (ly <= Y0 + 1.f && hy >= Y0) ? 1u : 0u;
+                    const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
+                    gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
                 }
             }
             const uint32_t m = __ballot_sync(0xffffffffu, gmask != 0);
