@@ -129,6 +129,21 @@ int splat_rasterize(const void *scene_const, int64_t n, const splat_view_t *view
 int splat_view_pack64(const void *scene_const, int64_t n, const splat_view_t *view, double *pack64,
                       void *stream);
 
+/* ---- reverse mode -------------------------------------------------------
+ * render_backward (raster_backward.py:73-153) for a frame rendered with
+ * train != 0 (its workspace still holds the bins): replays each pixel's
+ * contributors back to front (_kernels.backward_region, _kernels.py:132-365),
+ * reduces per-(splat, tile) partials in fixed order and chains them into the
+ * stored parametrisation.  adjoint = (H,W,4,3) [w, wx, wy, wxy] (PixelAdjoint).
+ * grads (float32, 11n) = [d_means (n,2) | d_log_scales (n,2) | d_rotations (n) |
+ * d_opacity_logits (n) | d_colors (n,3)] in storage order; accumulate != 0 adds. */
+size_t splat_backward_workspace_bytes(int64_t n, int64_t pair_capacity);
+int splat_render_backward(const void *scene_const, const splat_scene_t *scene /* host struct */,
+                          const splat_view_t *view /* host */, int width, int height,
+                          const splat_gimg_t *fwd /* host struct */, const float *adjoint, void *workspace,
+                          size_t ws_bytes, int64_t pair_capacity, void *bwd_workspace, size_t bwd_bytes,
+                          float *grads, int accumulate, void *stream);
+
 /* ---- spline upscaler ----------------------------------------------------
  * upscale_spline (spline.py:162-178): (H,W,4,3) gradient planes -> (Ho,Wo,3).
  * upscale_backward (spline.py:191-243): (Ho,Wo,3) adjoint -> (H,W,4,3). */

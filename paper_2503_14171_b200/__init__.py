@@ -11,6 +11,8 @@ from .core import (ALPHA_CLAMP, ALPHA_CULL, EARLY_TERMINATION, DegenerateCovaria
                    DimensionError, ParameterError, Scene, UnsupportedScaleError, logistic, logit)
 from .raster_forward import (GradientImage, RenderPack, bin_tiles, prepare_scene, render_forward,
                              sort_by_depth, tile_grid)
+from .raster_backward import (GradBuffer, PixelAdjoint, SceneGrads, invert_alpha_state,
+                              render_backward)
 from .scenes import View, random_views, synthetic_scene, view_scene
 from .spline import (SourceAdjoint, fd_gradients, fd_gradients_backward, upscale_backward,
                      upscale_spline)
@@ -21,6 +23,7 @@ __all__ = [
     "ALPHA_CLAMP", "ALPHA_CULL", "EARLY_TERMINATION", "DegenerateCovarianceError", "DimensionError",
     "ParameterError", "Scene", "UnsupportedScaleError", "logistic", "logit", "GradientImage",
     "RenderPack", "bin_tiles", "prepare_scene", "render_forward", "sort_by_depth", "tile_grid",
+    "GradBuffer", "PixelAdjoint", "SceneGrads", "invert_alpha_state", "render_backward",
     "View", "random_views", "synthetic_scene", "view_scene", "SourceAdjoint", "fd_gradients",
     "fd_gradients_backward", "upscale_backward", "upscale_spline",
 ]

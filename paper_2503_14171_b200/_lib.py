@@ -65,6 +65,9 @@ SIGNATURES = {
     "splat_rasterize": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
                               ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_view_pack64": (I32, [P, I64, ctypes.POINTER(ViewT), P, P]),
+    "splat_backward_workspace_bytes": (SZ, [I64, I64]),
+    "splat_render_backward": (I32, [P, ctypes.POINTER(SceneT), ctypes.POINTER(ViewT), I32, I32,
+                                    ctypes.POINTER(GimgT), P, P, SZ, I64, P, SZ, P, I32, P]),
     "splat_upscale_plan_bytes": (SZ, [I32, I32, I32, I32]),
     "splat_upscale_plan": (I32, [I32, I32, I32, I32, P, P]),
     "splat_upscale_forward": (I32, [P, I32, I32, P, I32, I32, I32, P, P]),

@@ -26,6 +26,10 @@ size_t scene_workspace_bytes_impl(int64_t n);
 int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaStream_t stream);
 bool sorted_in_alt(int ntiles);
 int launch_pack64(const SceneConst& sc, const ViewConst& vc, double* out, cudaStream_t stream);
+size_t backward_workspace_bytes_impl(int64_t n, int64_t cap);
+int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, const ViewConst& vc,
+                           const FrameLayout& L, char* ws, const splat_gimg_t& fwd, const float* adj,
+                           char* bws, float* grads, int accumulate, cudaStream_t stream);
 int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
                          int clamp, const void* plan, cudaStream_t stream);
 size_t upscale_plan_bytes_impl(int out_w, int out_h);
@@ -155,6 +159,27 @@ int splat_upscale_plan(int in_w, int in_h, int out_w, int out_h, void* plan, voi
     if (out_w < in_w || out_h < in_h)
         return set_error(SPLAT_ERR_SCALE, "output must be at least source size");
     return upscale_plan_impl(in_w, in_h, out_w, out_h, plan, (cudaStream_t)stream);
+}
+
+size_t splat_backward_workspace_bytes(int64_t n, int64_t pair_capacity) {
+    return backward_workspace_bytes_impl(n, pair_capacity);
+}
+
+int splat_render_backward(const void* scene_const, const splat_scene_t* scene, const splat_view_t* view,
+                          int width, int height, const splat_gimg_t* fwd, const float* adjoint, void* workspace,
+                          size_t ws_bytes, int64_t pair_capacity, void* bwd_workspace, size_t bwd_bytes,
+                          float* grads, int accumulate, void* stream) {
+    int rc = check_dims(width, height);
+    if (rc) return rc;
+    if (!fwd || !fwd->state || !fwd->last)
+        return set_error(SPLAT_ERR_PARAMETER, "backward needs a training-mode forward (state + last)");
+    FrameLayout L = frame_layout(scene->n, width, height, pair_capacity);
+    if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    if (bwd_bytes < backward_workspace_bytes_impl(scene->n, pair_capacity))
+        return set_error(SPLAT_ERR_PARAMETER, "backward workspace too small");
+    return launch_raster_backward(scene_const_view(scene_const, scene->n), *scene, make_view_const(*view), L,
+                                  (char*)workspace, *fwd, adjoint, (char*)bwd_workspace, grads, accumulate,
+                                  (cudaStream_t)stream);
 }
 
 int splat_upscale_forward(const float* src, int in_w, int in_h, float* out, int out_w, int out_h, int clamp,

@@ -1,0 +1,348 @@
+// Reverse-mode rasterizer (sm_100a): _kernels.backward_region
+// (_kernels.py:132-365) + the fixed-order reduction and parametrisation chain
+// of render_backward (raster_backward.py:87-152).
+//
+// Per pixel (lane) the contributor list is replayed back to front from the
+// forward's `last` index with the same certified decisions and canonical
+// float32 footprint values as the forward pass, so the replay is exact.  The
+// accumulated-alpha state is inverted in float64 starting from the private
+// float64 terminal state the training forward wrote:
+//   T_{k-1} = T_k / om_k,  A_{x,k-1} = (A_{x,k} - T_{k-1} a_x) / om_k, ...
+// Gradients are reduced without atomics: butterfly shuffles within a warp,
+// then a fixed warp order in shared memory, into one partial per (tile,
+// splat) pair; `reduce_pairs_kernel` sums each splat's pairs in tile order.
+#include <cmath>
+
+#include "footprint.cuh"
+
+namespace splat {
+
+namespace {
+
+constexpr int kBwBatch = 32;
+constexpr int kWarps_bw = kBlock / 32;
+constexpr int kG = 9;   // d_color(3), d_sigma, d_mean(2), d_conic(3)
+
+struct BwdArgs {
+    SceneConst sc;
+    ViewConst vc;
+    int width, height, ntx;
+    const uint32_t* ranges;
+    const uint32_t* ranks;
+    const PackF* pack;
+    const short4* bboxes;
+    const uint32_t* offsets;   // pair offset of each rank (emission order)
+    const uint32_t* last;
+    const int32_t* count;
+    const double* state;       // (H,W,4) terminal T, A_x, A_y, A_xy
+    const float* adj;          // (H,W,4,3) w, wx, wy, wxy
+    float* partial;            // (pairs, 9) per (splat, tile) partial, emission order
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+__global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
+    __shared__ PackF s_pack[kWarps_bw][kBwBatch];
+    __shared__ float4 s_col[kWarps_bw][kBwBatch];
+    __shared__ uint32_t s_rank[kWarps_bw][kBwBatch];
+    __shared__ float s_part[kWarps_bw][kBwBatch][kG];
+    __shared__ uint32_t s_touch[kWarps_bw];
+    __shared__ uint32_t s_hi[kWarps_bw];
+
+    const int tile = blockIdx.x;
+    const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rx0 = tile_x * kTile + (warp & 1) * 8, ry0 = tile_y * kTile + (warp >> 1) * 4;
+    const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3);
+    const bool inside = px < p.width && py < p.height;
+    const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
+    const float X0 = (float)rx0 + 0.5f, Y0 = (float)ry0 + 0.5f;
+    const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
+
+    // per-pixel inputs
+    const int64_t o = (int64_t)py * p.width + px;
+    uint32_t my_last = start;
+    float w[12];
+    double T = 1.0, ax = 0.0, ay = 0.0, axy = 0.0;
+    bool live = false;
+    if (inside) {
+        my_last = p.last[o];
+        const float4* a4 = reinterpret_cast<const float4*>(p.adj + 12 * o);
+        const float4 w0 = a4[0], w1 = a4[1], w2 = a4[2];
+        w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
+        w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+        w[8] = w2.x; w[9] = w2.y; w[10] = w2.z; w[11] = w2.w;
+        bool nz = false;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) nz |= (w[i] != 0.f);
+        live = nz && p.count[o] > 0;   // _kernels.py:155-174
+        const double2* st = reinterpret_cast<const double2*>(p.state + 4 * o);
+        const double2 s0 = st[0], s1 = st[1];
+        T = s0.x;
+        ax = s0.y;
+        ay = s1.x;
+        axy = s1.y;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 12; ++i) w[i] = 0.f;
+    }
+    // behind-colour state, the background acting as a far splat (_kernels.py:218-229)
+    float bh[3] = {p.vc.bg[0], p.vc.bg[1], p.vc.bg[2]};
+    float bhx[3] = {0.f, 0.f, 0.f}, bhy[3] = {0.f, 0.f, 0.f}, bhxy[3] = {0.f, 0.f, 0.f};
+
+    // block-wide highest list end among live pixels
+    uint32_t hi = live ? my_last : start;
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (lane == 0) s_hi[warp] = hi;
+    __syncthreads();
+    hi = start;
+#pragma unroll
+    for (int k = 0; k < kWarps_bw; ++k) hi = max(hi, s_hi[k]);
+
+    for (uint32_t top = hi; top > start; top = (top - start > (uint32_t)kBwBatch) ? top - kBwBatch : start) {
+        const uint32_t lo = (top - start > (uint32_t)kBwBatch) ? top - kBwBatch : start;
+        const int nb = (int)(top - lo);
+        // every warp stages the batch and culls it against its own rectangle
+        const uint32_t j = lo + lane;
+        bool keep = false;
+        if (lane < nb) {
+            const uint32_t r = p.ranks[j];
+            const PackF g = p.pack[r];
+            keep = ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f);
+            s_pack[warp][lane] = g;
+            s_col[warp][lane] = p.sc.color[r];
+            s_rank[warp][lane] = r;
+        }
+        uint32_t bits = __ballot_sync(0xffffffffu, keep);
+        uint32_t touched = 0;
+        __syncwarp();
+        while (bits) {
+            const int k = 31 - __clz(bits);   // back to front
+            bits &= ~(1u << k);
+            const uint32_t jk = lo + k;
+            float gr[kG];
+#pragma unroll
+            for (int i = 0; i < kG; ++i) gr[i] = 0.f;
+            bool contrib = false;
+            if (live && jk < my_last) {
+                const PackF g = s_pack[warp][k];
+                float al, gax, gay, gaxy, rel;
+                int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
+                if (st == kUnsure) {
+                    double a64;
+                    st = eval_exact(p.sc, p.vc, p.bboxes, s_rank[warp][k], px, py, &a64);
+                    if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
+                }
+                if (st != kCulled) {
+                    contrib = true;
+                    const float4 col = s_col[warp][k];
+                    const float cc[3] = {col.x, col.y, col.z};
+                    // invert the accumulated-alpha state across this splat (float64)
+                    const double om = st == kClamped ? (double)1.0e-3f : (double)(1.f - al);
+                    const double inv = 1.0 / om;
+                    const double Tp = T * inv;
+                    const double axp = (ax - Tp * (double)gax) * inv;
+                    const double ayp = (ay - Tp * (double)gay) * inv;
+                    const double axyp = (axy - Tp * (double)gaxy + axp * (double)gay + ayp * (double)gax) * inv;
+                    const float t = (float)Tp, sx = (float)axp, sy = (float)ayp, sxy = (float)axyp;
+                    float abar = 0.f, abar_x = 0.f, abar_y = 0.f, abar_xy = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float W0 = w[c], WX = w[3 + c], WY = w[6 + c], WXY = w[9 + c];
+                        const float diff = cc[c] - bh[c];
+                        const float u0 = t * diff;
+                        const float u1 = -sx * diff - t * bhx[c];
+                        const float u2 = -sy * diff - t * bhy[c];
+                        const float u3 = ((-sxy * diff + sx * bhy[c]) + sy * bhx[c]) - t * bhxy[c];
+                        // _kernels.py:253-262
+                        gr[c] = W0 * (t * al) + WX * (t * gax - sx * al) + WY * (t * gay - sy * al) +
+                                WXY * (((t * gaxy - sxy * al) - sy * gax) - sx * gay);
+                        abar += W0 * u0 + WX * u1 + WY * u2 + WXY * u3;
+                        abar_x += WX * u0 + WXY * u2;
+                        abar_y += WY * u0 + WXY * u1;
+                        abar_xy += WXY * u0;
+                    }
+                    if (st != kClamped) {   // _kernels.py:291-336
+                        const float dx = (cx - g.mxh) - g.mxl, dy = (cy - g.myh) - g.myl;
+                        const float ca = g.a, cb = g.b, ccn = g.c;
+                        const float gx = -(2.f * ca * dx + 2.f * cb * dy);
+                        const float gy = -(2.f * cb * dx + 2.f * ccn * dy);
+                        const float hxy = gx * gy - 2.f * cb;
+                        gr[3] = abar * al + abar_x * gax + abar_y * gay + abar_xy * gaxy;   // / sigma later
+                        gr[4] = al * (abar * (-gx) + abar_x * (-gx * gx + 2.f * ca) + abar_y * (-gx * gy + 2.f * cb) +
+                                      abar_xy * (-gx * hxy + 2.f * ca * gy + 2.f * cb * gx));
+                        gr[5] = al * (abar * (-gy) + abar_x * (-gy * gx + 2.f * cb) + abar_y * (-gy * gy + 2.f * ccn) +
+                                      abar_xy * (-gy * hxy + 2.f * cb * gy + 2.f * ccn * gx));
+                        const float dxx = dx * dx, dxy2 = 2.f * dx * dy, dyy = dy * dy;
+                        gr[6] = al * (abar * (-dxx) + abar_x * (-dxx * gx - 2.f * dx) + abar_y * (-dxx * gy) +
+                                      abar_xy * (-dxx * hxy - 2.f * dx * gy));
+                        gr[7] = al * (abar * (-dxy2) + abar_x * (-dxy2 * gx - 2.f * dy) +
+                                      abar_y * (-dxy2 * gy - 2.f * dx) +
+                                      abar_xy * (((-dxy2 * hxy - 2.f * dy * gy) - 2.f * gx * dx) - 2.f));
+                        gr[8] = al * (abar * (-dyy) + abar_x * (-dyy * gx) + abar_y * (-dyy * gy - 2.f * dy) +
+                                      abar_xy * (-dyy * hxy - 2.f * dy * gx));
+                    }
+                    // advance the behind-colour state through this splat (_kernels.py:337-357)
+                    const float omf = (float)om;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float dcb = cc[c] - bh[c];
+                        const float nbx = omf * bhx[c] + gax * dcb;
+                        const float nby = omf * bhy[c] + gay * dcb;
+                        const float nbxy = ((omf * bhxy[c] + gaxy * dcb) - gay * bhx[c]) - gax * bhy[c];
+                        bh[c] = omf * bh[c] + al * cc[c];
+                        bhx[c] = nbx;
+                        bhy[c] = nby;
+                        bhxy[c] = nbxy;
+                    }
+                    T = Tp;
+                    ax = axp;
+                    ay = ayp;
+                    axy = axyp;
+                }
+            }
+            if (__any_sync(0xffffffffu, contrib)) {
+#pragma unroll
+                for (int i = 0; i < kG; ++i) gr[i] = warp_sum(gr[i]);
+                if (lane == 0) {
+#pragma unroll
+                    for (int i = 0; i < kG; ++i) s_part[warp][k][i] = gr[i];
+                }
+                touched |= 1u << k;
+            }
+        }
+        if (lane == 0) s_touch[warp] = touched;
+        __syncthreads();
+        // fixed warp order: one partial per (splat, tile) pair, written at the pair's
+        // emission slot offsets[r] + (tile index within the splat's tile rectangle)
+        if (tid < nb) {
+            float acc[kG];
+#pragma unroll
+            for (int i = 0; i < kG; ++i) acc[i] = 0.f;
+            bool any = false;
+#pragma unroll
+            for (int ww = 0; ww < kWarps_bw; ++ww) {
+                if ((s_touch[ww] >> tid) & 1u) {
+                    any = true;
+#pragma unroll
+                    for (int i = 0; i < kG; ++i) acc[i] += s_part[ww][tid][i];
+                }
+            }
+            if (any) {
+                const uint32_t r = s_rank[0][tid];
+                const short4 bb = p.bboxes[r];
+                const int btx0 = bb.x / kTile, bty0 = bb.z / kTile, bnx = (bb.y - 1) / kTile - btx0 + 1;
+                const uint32_t slot = p.offsets[r] + (uint32_t)((tile_y - bty0) * bnx + (tile_x - btx0));
+                float* dst = p.partial + (size_t)slot * kG;
+#pragma unroll
+                for (int i = 0; i < kG; ++i) dst[i] = acc[i];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Per splat (rank): sum its pair partials in tile order (raster_backward.py:116-124).
+__global__ void reduce_pairs_kernel(int64_t n, const uint32_t* __restrict__ touched,
+                                    const uint32_t* __restrict__ offsets, const float* __restrict__ partial,
+                                    int64_t cap, float* __restrict__ g9) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    float acc[kG];
+#pragma unroll
+    for (int i = 0; i < kG; ++i) acc[i] = 0.f;
+    const uint32_t off = offsets[r], cnt = touched[r];
+    for (uint32_t k = 0; k < cnt; ++k) {
+        if ((int64_t)(off + k) >= cap) break;
+        const float* src = partial + (size_t)(off + k) * kG;
+#pragma unroll
+        for (int i = 0; i < kG; ++i) acc[i] += src[i];
+    }
+#pragma unroll
+    for (int i = 0; i < kG; ++i) g9[(size_t)r * kG + i] = acc[i];
+}
+
+// Render-space -> stored parametrisation (raster_backward.py:126-152), scattered
+// back to storage order.  grads layout (float32, n = scene size):
+//   [d_means (n,2) | d_log_scales (n,2) | d_rotations (n) | d_opacity_logits (n) | d_colors (n,3)]
+__global__ void chain_kernel(int64_t n, const int32_t* __restrict__ order, const double* __restrict__ ls,
+                             const double* __restrict__ rot, const double* __restrict__ sigma_r,
+                             const float* __restrict__ g9, double kx, double ky, int accumulate,
+                             float* __restrict__ grads) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int64_t s = order[r];
+    const float* g = g9 + (size_t)r * kG;
+    const double sg = sigma_r[r];
+    const double d_sigma = (double)g[3] / sg;
+    const double dn00 = (double)g[6] / (2.0 * kx * kx);
+    const double dn01 = (double)g[7] / (2.0 * kx * ky);
+    const double dn11 = (double)g[8] / (2.0 * ky * ky);
+    const double e1 = exp(-2.0 * ls[2 * s]), e2 = exp(-2.0 * ls[2 * s + 1]);
+    double sn, c;
+    sincos(rot[s], &sn, &c);
+    const double d_l1 = -2.0 * e1 * (dn00 * c * c + dn01 * sn * c + dn11 * sn * sn);
+    const double d_l2 = -2.0 * e2 * (dn00 * sn * sn - dn01 * sn * c + dn11 * c * c);
+    const double sin2 = 2.0 * sn * c, cos2 = c * c - sn * sn;
+    const double d_rot = (e2 - e1) * sin2 * dn00 + (e1 - e2) * cos2 * dn01 + (e1 - e2) * sin2 * dn11;
+    float* gm = grads;
+    float* gl = grads + 2 * n;
+    float* gr = grads + 4 * n;
+    float* go = grads + 5 * n;
+    float* gc = grads + 6 * n;
+    const float v[9] = {(float)((double)g[4] * kx), (float)((double)g[5] * ky), (float)d_l1, (float)d_l2,
+                         (float)d_rot, (float)(d_sigma * sg * (1.0 - sg)), g[0], g[1], g[2]};
+    float* dst[9] = {gm + 2 * s, gm + 2 * s + 1, gl + 2 * s, gl + 2 * s + 1, gr + s, go + s,
+                     gc + 3 * s, gc + 3 * s + 1, gc + 3 * s + 2};
+#pragma unroll
+    for (int i = 0; i < 9; ++i) *dst[i] = accumulate ? *dst[i] + v[i] : v[i];
+}
+
+}  // namespace
+
+size_t backward_workspace_bytes_impl(int64_t n, int64_t cap) {
+    size_t nn = (size_t)(n > 0 ? n : 1), cc = (size_t)(cap > 0 ? cap : 1);
+    return ((cc * kG * 4 + 255) & ~size_t(255)) + nn * kG * 4;
+}
+
+int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, const ViewConst& vc,
+                           const FrameLayout& L, char* ws, const splat_gimg_t& fwd, const float* adj,
+                           char* bws, float* grads, int accumulate, cudaStream_t stream) {
+    extern bool sorted_in_alt(int ntiles);
+    const size_t nn = (size_t)(L.n > 0 ? L.n : 1), cc = (size_t)(L.cap > 0 ? L.cap : 1);
+    float* partial = (float*)bws;
+    float* g9 = (float*)(bws + ((cc * kG * 4 + 255) & ~size_t(255)));
+    if (L.n == 0) return SPLAT_OK;
+    SPLAT_CUDA_CHECK(cudaMemsetAsync(partial, 0, cc * kG * 4, stream));
+    BwdArgs a;
+    a.sc = sc;
+    a.vc = vc;
+    a.width = L.width;
+    a.height = L.height;
+    a.ntx = L.ntx;
+    a.ranges = (const uint32_t*)(ws + L.ranges);
+    bool alt = sorted_in_alt(L.ntx * L.nty);
+    a.ranks = (const uint32_t*)(ws + (alt ? L.vals1 : L.vals0));
+    a.pack = (const PackF*)(ws + L.pack);
+    a.bboxes = (const short4*)(ws + L.bboxes);
+    a.offsets = (const uint32_t*)(ws + L.offsets);
+    a.last = fwd.last;
+    a.count = fwd.count;
+    a.state = fwd.state;
+    a.adj = adj;
+    a.partial = partial;
+    raster_bwd_kernel<<<L.ntx * L.nty, kBlock, 0, stream>>>(a); note_launch();
+    const int blocks = (int)((L.n + 255) / 256);
+    reduce_pairs_kernel<<<blocks, 256, 0, stream>>>(L.n, (const uint32_t*)(ws + L.touched),
+                                                    (const uint32_t*)(ws + L.offsets), partial, L.cap, g9); note_launch();
+    chain_kernel<<<blocks, 256, 0, stream>>>(L.n, sc.order, scene.log_scales, scene.rotations, sc.sigma, g9,
+                                             vc.kx, vc.ky, accumulate, grads); note_launch();
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
+
+}  // namespace splat

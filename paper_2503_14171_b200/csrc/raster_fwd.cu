@@ -18,13 +18,11 @@
 // contributor list) therefore equal the reference's; values are float32.
 #include <cmath>
 
-#include "kernels.cuh"
+#include "footprint.cuh"
 
 namespace splat {
 
 namespace {
-
-enum : int { kCulled = 0, kContrib = 1, kClamped = 2, kUnsure = 3 };
 
 struct RasterArgs {
     SceneConst sc;
@@ -42,118 +40,6 @@ struct RasterArgs {
     uint32_t* fixup;
     uint32_t* counters;
 };
-
-// Exact reference evaluation of one candidate at one pixel centre
-// (_kernels.py:61-80, float64, every operation individually rounded).
-__device__ __forceinline__ int eval_exact_inl(const SceneConst& sc, const ViewConst& vc,
-                                              const short4* bboxes, uint32_t r, int px, int py,
-                                              double* alpha64) {
-    short4 bb = bboxes[r];
-    if (px < bb.x || px >= bb.y || py < bb.z || py >= bb.w) return kCulled;
-    double mx = __dmul_rn(__dsub_rn(sc.mean[2 * r], vc.ox), vc.kx);
-    double my = __dmul_rn(__dsub_rn(sc.mean[2 * r + 1], vc.oy), vc.ky);
-    double ca = __ddiv_rn(sc.n00[r], vc.c00);
-    double cb = __ddiv_rn(sc.n01[r], vc.c01);
-    double cc = __ddiv_rn(sc.n11[r], vc.c11);
-    double dx = __dsub_rn((double)px + 0.5, mx);
-    double dy = __dsub_rn((double)py + 0.5, my);
-    double t1 = __dmul_rn(__dmul_rn(ca, dx), dx);
-    double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, cb), dx), dy);
-    double t3 = __dmul_rn(__dmul_rn(cc, dy), dy);
-    double expo = -__dadd_rn(__dadd_rn(t1, t2), t3);
-    if (expo < kLogCull) return kCulled;
-    double araw = __dmul_rn(sc.sigma[r], exp(expo));
-    if (araw < kAlphaCull) return kCulled;
-    if (araw > kAlphaClamp) {
-        *alpha64 = kAlphaClamp;
-        return kClamped;
-    }
-    *alpha64 = araw;
-    return kContrib;
-}
-
-// Out-of-line copy for the main pass, where the exact path is rare and must
-// not inflate the register footprint of the hot loop.
-__device__ __noinline__ int eval_exact(const SceneConst& sc, const ViewConst& vc, const short4* bboxes,
-                                       uint32_t r, int px, int py, double* alpha64) {
-    return eval_exact_inl(sc, vc, bboxes, r, px, py, alpha64);
-}
-
-// 2^x via MUFU.EX2 (flush-to-zero: results below 2^-126 are far below the cull).
-// Max relative error 2^-22, inside the 2^-20 budget of eval_fast's `rel`.
-__device__ __forceinline__ float fast_exp2(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-__device__ __forceinline__ float fast_rcp(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-// Float32 footprint with a certified decision (_kernels.py:65-87).  Returns
-// kCulled / kContrib / kClamped when the float32 evaluation decides the
-// reference's tests with margin, kUnsure otherwise.  `al` etc. are the
-// canonical float32 values used for blending (identical in the backward pass);
-// `rel` receives the relative error bound of `al`.
-__device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, float& al, float& ax,
-                                         float& ay, float& axy, float& rel) {
-    float dx = (cx - g.mxh) - g.mxl;
-    float dy = (cy - g.myh) - g.myl;
-    float adx = g.a * dx;
-    float b2 = 2.f * g.b;
-    float t1 = adx * dx;
-    float t2 = (b2 * dx) * dy;
-    float t3 = (g.c * dy) * dy;
-    float qf = (t1 + t2) + t3;
-    float s = (t1 + fabsf(t2)) + t3;
-    // |qf - Q_exact| <= ~8 ulp * s; conic/mean rounding adds ~4 ulp * s.  2^-19 * s is a 2x margin.
-    float tol = fmaf(s + g.qcull, 1.9073486e-06f, 1e-30f);
-    // |al - alpha_ref| / al <= 2^-21 s (Q) + 2^-20 (exp2 approx, log2e product, sigma, product)
-    rel = fmaf(s, 4.7683716e-07f, 9.5367432e-07f);
-    if (qf > g.qcull + tol) return kCulled;
-    if (qf >= g.qcull - tol) return kUnsure;
-    if (qf <= g.qclamp + tol) {
-        if (qf < g.qclamp - tol) {
-            al = 0.999f;
-            ax = 0.f;
-            ay = 0.f;
-            axy = 0.f;
-            return kClamped;
-        }
-        return kUnsure;
-    }
-    al = g.sigma * fast_exp2(-1.44269504f * qf);
-    float gx = -2.f * fmaf(g.b, dy, adx);
-    float gy = -2.f * fmaf(g.b, dx, g.c * dy);
-    ax = al * gx;
-    ay = al * gy;
-    axy = al * fmaf(gx, gy, -b2);
-    return kContrib;
-}
-
-// Values of a candidate whose decision came from the exact path.
-__device__ __forceinline__ void canonical_values(const PackF& g, float cx, float cy, int st, float& al,
-                                                 float& ax, float& ay, float& axy) {
-    if (st == kClamped) {
-        al = 0.999f;
-        ax = ay = axy = 0.f;
-        return;
-    }
-    float dx = (cx - g.mxh) - g.mxl;
-    float dy = (cy - g.myh) - g.myl;
-    float adx = g.a * dx;
-    float b2 = 2.f * g.b;
-    float qf = ((adx * dx) + ((b2 * dx) * dy)) + ((g.c * dy) * dy);
-    al = g.sigma * fast_exp2(-1.44269504f * qf);
-    float gx = -2.f * fmaf(g.b, dy, adx);
-    float gy = -2.f * fmaf(g.b, dx, g.c * dy);
-    ax = al * gx;
-    ay = al * gy;
-    axy = al * fmaf(gx, gy, -b2);
-}
 
 // Per-pixel blend state (_kernels.py:41-57 accumulators).  T is the
 // transmittance 1 - A; TRAIN keeps the A-state in float64 for the backward
@@ -229,33 +115,6 @@ struct Blend {
         ++n;
     }
 };
-
-// Conservative "does the cull ellipse {Q <= qcull} reach the pixel-centre
-// rectangle [X0,X1] x [Y0,Y1]" test.  The minimum of the positive-definite
-// form over the rectangle is at the centre (if inside) or on an edge, where it
-// is a 1-D quadratic minimised in closed form.  Each edge value is lowered by
-// a bound on its float32 error (2^-18 (a u^2 + c v^2) >= 8 ulp * s) before the
-// comparison, and NaNs keep the candidate, so no contributing candidate is
-// ever rejected.  pad0/pad1 of the pack hold b/a and b/c.
-__device__ __forceinline__ bool ellipse_hits_rect(const PackF& g, float X0, float X1, float Y0, float Y1) {
-    const float u0 = (X0 - g.mxh) - g.mxl, u1 = (X1 - g.mxh) - g.mxl;
-    const float v0 = (Y0 - g.myh) - g.myl, v1 = (Y1 - g.myh) - g.myl;
-    if (u0 <= 0.f && u1 >= 0.f && v0 <= 0.f && v1 >= 0.f) return true;
-    const float b2 = 2.f * g.b;
-    float lo = 3.0e38f;
-    auto edge = [&](float u, float v) {
-        float t1 = (g.a * u) * u, t3 = (g.c * v) * v;
-        float qv = fmaf(b2 * u, v, t1 + t3);
-        lo = fminf(lo, fmaf(-(t1 + t3), 3.8146973e-06f, qv));
-    };
-    // vertical edges u = u0, u1: v* = -(b/c) u clamped
-    edge(u0, fminf(fmaxf(-g.pad1 * u0, v0), v1));
-    edge(u1, fminf(fmaxf(-g.pad1 * u1, v0), v1));
-    // horizontal edges v = v0, v1: u* = -(b/a) v clamped
-    edge(fminf(fmaxf(-g.pad0 * v0, u0), u1), v0);
-    edge(fminf(fmaxf(-g.pad0 * v1, u0), u1), v1);
-    return !(lo > fmaf(g.qcull, 3.8146973e-06f, g.qcull));
-}
 
 template <bool TRAIN>
 __device__ __forceinline__ void write_pixel(const RasterArgs& p, int px, int py, const Blend<TRAIN>& s) {
