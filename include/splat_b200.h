@@ -144,6 +144,18 @@ int splat_render_backward(const void *scene_const, const splat_scene_t *scene /*
                           size_t ws_bytes, int64_t pair_capacity, void *bwd_workspace, size_t bwd_bytes,
                           float *grads, int accumulate, void *stream);
 
+/* ---- training loss and optimizer ----------------------------------------
+ * loss (fit.py:94-108) with ssim_with_grad (baselines.py:170-203):
+ * value[0] = (1-l) L1 + l (1 - SSIM), value[1] = SSIM (device float64);
+ * adjoint (H,W,3) = dL/dpred.  pred/target are (H,W,3) float32. */
+size_t splat_loss_workspace_bytes(int width, int height);
+int splat_loss(const float *pred, const float *target, int width, int height, double ssim_weight,
+               float *adjoint, double *value, void *workspace, size_t ws_bytes, void *stream);
+/* adam_step (fit.py:144-160) on one parameter group: float64 params and
+ * moments, float32 gradients; bc1/bc2 = 1 - beta^t computed by the caller. */
+int splat_adam_step(double *params, const float *grads, double *m, double *v, int64_t count, double lr,
+                    double beta1, double beta2, double bc1, double bc2, double eps, void *stream);
+
 /* ---- spline upscaler ----------------------------------------------------
  * upscale_spline (spline.py:162-178): (H,W,4,3) gradient planes -> (Ho,Wo,3).
  * upscale_backward (spline.py:191-243): (Ho,Wo,3) adjoint -> (H,W,4,3). */

@@ -27,6 +27,11 @@ int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaSt
 bool sorted_in_alt(int ntiles);
 int launch_pack64(const SceneConst& sc, const ViewConst& vc, double* out, cudaStream_t stream);
 size_t backward_workspace_bytes_impl(int64_t n, int64_t cap);
+size_t loss_workspace_bytes_impl(int w, int h);
+int loss_impl(const float* pred, const float* target, int w, int h, double lam, float* adj, double* value,
+              void* ws, cudaStream_t stream);
+int adam_impl(double* p, const float* g, double* m, double* v, int64_t count, double lr, double b1, double b2,
+              double bc1, double bc2, double eps, cudaStream_t stream);
 int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, const ViewConst& vc,
                            const FrameLayout& L, char* ws, const splat_gimg_t& fwd, const float* adj,
                            char* bws, float* grads, int accumulate, cudaStream_t stream);
@@ -180,6 +185,24 @@ int splat_render_backward(const void* scene_const, const splat_scene_t* scene, c
     return launch_raster_backward(scene_const_view(scene_const, scene->n), *scene, make_view_const(*view), L,
                                   (char*)workspace, *fwd, adjoint, (char*)bwd_workspace, grads, accumulate,
                                   (cudaStream_t)stream);
+}
+
+size_t splat_loss_workspace_bytes(int width, int height) { return loss_workspace_bytes_impl(width, height); }
+
+int splat_loss(const float* pred, const float* target, int width, int height, double ssim_weight, float* adjoint,
+               double* value, void* workspace, size_t ws_bytes, void* stream) {
+    if (width <= 0 || height <= 0) return set_error(SPLAT_ERR_DIMENSION, "empty image");
+    if (ssim_weight < 0.0 || ssim_weight > 1.0) return set_error(SPLAT_ERR_PARAMETER, "ssim_weight must be in [0, 1]");
+    if (ssim_weight > 0.0 && (width < 11 || height < 11))
+        return set_error(SPLAT_ERR_DIMENSION, "ssim requires images of at least 11 pixels per side");
+    if (ws_bytes < loss_workspace_bytes_impl(width, height))
+        return set_error(SPLAT_ERR_PARAMETER, "loss workspace too small");
+    return loss_impl(pred, target, width, height, ssim_weight, adjoint, value, workspace, (cudaStream_t)stream);
+}
+
+int splat_adam_step(double* params, const float* grads, double* m, double* v, int64_t count, double lr,
+                    double beta1, double beta2, double bc1, double bc2, double eps, void* stream) {
+    return adam_impl(params, grads, m, v, count, lr, beta1, beta2, bc1, bc2, eps, (cudaStream_t)stream);
 }
 
 int splat_upscale_forward(const float* src, int in_w, int in_h, float* out, int out_w, int out_h, int clamp,
