@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--slots", type=int, default=4, help="concurrent view streams in the timed region")
     ap.add_argument("--kernel-views", type=int, default=64,
                     help="views of the single-stream per-kernel timing pass (roofline)")
+    ap.add_argument("--workload", default="render", choices=["render", "train"],
+                    help="render: C3 frames/s (headline); train: C5 upscale-aware training step")
+    ap.add_argument("--train-views", type=int, default=4, help="views per rank per training step (C5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -169,10 +172,124 @@ class ClockSampler:
 # our arm
 # ---------------------------------------------------------------------------
 
+def train_workload(views_per_rank, world):
+    from paper_2503_14171_b200.scenes import CONFIGS, random_views, synthetic_scene
+    c = CONFIGS["c5"]
+    model = synthetic_scene(c.n, c.canvas_w, c.canvas_h, c.scale_range, seed=5)
+    target = synthetic_scene(c.n, c.canvas_w, c.canvas_h, c.scale_range, seed=7)
+    views = random_views(views_per_rank * world, c.canvas_w, c.canvas_h, seed=13)
+    return c, model, target, views
+
+
+TRAIN_METRIC = "upscale-aware training view-steps/s (C5: 1M splats, 480x270 render, x4 to 1920x1080, L1+SSIM)"
+
+
+def train_config(c, world, vpr):
+    return {"workload": "c5: 1M-splat model (seed 5) fit to a 1M-splat target scene (seed 7); per view: "
+                        "480x270 render with analytic gradients, x4 spline upscale to 1920x1080, "
+                        "L1+SSIM (lambda 0.2) loss, backward through upscaler and rasterizer; "
+                        "grads all-reduced over ranks, then Adam",
+            "n_splats": c.n, "render": [c.width, c.height], "output": list(c.out_size),
+            "views_per_rank": vpr, "parallelism": f"view-DP x{world} + NCCL all_reduce(SUM) of 11N fp32 grads"}
+
+
+def cpu_reference_train_view(model, target_img, view, c):
+    """One C5 view-step through the CPU oracle: fwd, upscale, loss, upscale bwd, raster bwd (seconds)."""
+    from oracle import oracle as O
+    from paper_2503_14171_b200.scenes import view_scene
+    t0 = time.perf_counter()
+    sc = view_scene(model, view)
+    fwd = O.render_forward(sc, c.width, c.height)
+    pred = O.upscale_spline(fwd.color, fwd.d_dx, fwd.d_dy, fwd.d_dxdy, c.factor, out_size=c.out_size)
+    _, dpred = O.loss(pred, target_img, 0.2)
+    sadj = O.upscale_backward(c.width, c.height, c.factor, dpred, out_size=c.out_size)
+    O.render_backward(sc, fwd, sadj)
+    return time.perf_counter() - t0
+
+
+def run_train(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2503_14171_b200 import _lib, distributed as D, fit
+    from paper_2503_14171_b200.raster_forward import render_forward
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    vpr = args.train_views
+    c, model, target_scene, views = train_workload(vpr, world)
+    mine = D.shard(views, rank, world)
+    W, H = c.out_size
+    targets = [render_forward(target_scene, W, H, view=v).color.clamp(0.0, 1.0).contiguous() for v in mine]
+    trainer = fit.ViewTrainer(model, (c.width, c.height), (W, H), mine, targets, ssim_weight=0.2)
+    for _ in range(args.warmup):
+        trainer.step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = lib.splat_kernel_launches()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(args.steps):
+        vals = trainer.step()
+    s1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = lib.splat_kernel_launches() - l0
+    ms = D.max_over_ranks(s0.elapsed_time(s1) / args.steps, device="cuda")
+    total_views = D.total_items(len(mine), device="cuda")
+    value = total_views / (ms / 1e3)
+    # e2e: targets streamed from pinned host memory every step, losses read back
+    host_t = [t.cpu().pin_memory() for t in targets]
+    h2d = sum(t.numel() * t.element_size() for t in host_t)
+    e0 = time.perf_counter()
+    ksteps = max(1, min(args.steps, 3))
+    for _ in range(ksteps):
+        for i, t in enumerate(host_t):
+            trainer.targets[i].copy_(t, non_blocking=True)
+        vals = trainer.step()
+        losses = vals.cpu()
+    torch.cuda.synchronize()
+    ems = D.max_over_ranks((time.perf_counter() - e0) / ksteps * 1e3, device="cuda")
+    clk = clocks.stop()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        O.build()
+        tgt0 = targets[0].double().cpu().numpy()
+        tcpu = cpu_reference_train_view(model, tgt0, mine[0], c)
+        cpu = {"value": 1.0 / tcpu, "unit": "view-steps/s", "cores": O.default_threads(), "kind": "port",
+               "sample": "1 C5 view-step (fwd, x4 upscale, L1+SSIM, upscale bwd, raster bwd) through the oracle"}
+    if rank == 0:
+        line = {"metric": TRAIN_METRIC, "value": value, "unit": "view-steps/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": train_config(c, world, vpr), "gpu_launches": int(launches),
+                "loss_last_step": [float(x) for x in losses[:, 0]],
+                "cpu_baseline": cpu,
+                "e2e": {"value": total_views / (ems / 1e3), "unit": "view-steps/s", "h2d_bytes_per_step": int(h2d),
+                        "d2h_bytes_per_step": int(vals.numel() * 8), "steps": ksteps},
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.workload == "train":
+        run_train(args)
         return
     import torch
     import torch.distributed as dist

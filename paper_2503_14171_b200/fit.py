@@ -25,9 +25,12 @@ import torch
 from . import _lib
 from .core import DimensionError, ParameterError
 from .device import DeviceScene, to_device
+from .distributed import allreduce_grads
 from .raster_backward import GradBuffer, PixelAdjoint, render_backward
 from .raster_forward import render_forward
-from .spline import upscale_backward, upscale_spline
+from .spline import fd_gradients, fd_gradients_backward, upscale_backward, upscale_spline
+
+UPSCALE_MODES = ("spline_analytic", "bicubic_fd")   # fit.py:23 (minus "none": no upscaling)
 
 DEFAULT_LEARNING_RATES = {       # fit.py:25-31
     "means": 2e-3,               # in normalized image units; scaled by max(W, H)
@@ -142,6 +145,8 @@ class ViewTrainer:
 
     def __post_init__(self):
         self.ds = to_device(self.scene)
+        if self.upscale_mode not in UPSCALE_MODES:
+            raise ParameterError(f"upscale_mode must be one of {UPSCALE_MODES}")
         if len(self.targets) != len(self.views):
             raise ParameterError("one target per view")
         w, h = self.out_size
@@ -158,13 +163,18 @@ class ViewTrainer:
         self.grads.zero_()
         for i, (v, tgt) in enumerate(zip(self.views, self.targets)):
             fwd = render_forward(ds, rw, rh, view=v, train=True)
-            pred = upscale_spline(fwd, 1.0, out_size=(w, h))
+            # fit.py:192-212: the analytic channels, or classical bicubic from FD planes
+            src = fwd if self.upscale_mode == "spline_analytic" else fd_gradients(fwd.color)
+            pred = upscale_spline(src, 1.0, out_size=(w, h))
             loss_device(pred, tgt, self.ssim_weight, adj=self._adj, value=self.values[i])
-            sadj = upscale_backward(fwd, 1.0, self._adj, out_size=(w, h))
-            render_backward(ds, fwd, PixelAdjoint.from_source(sadj), out=self.grads, accumulate=True,
-                            check_finite=False)
-        if self.group is not None:
-            torch.distributed.all_reduce(self.grads.flat, op=torch.distributed.ReduceOp.SUM, group=self.group)
+            sadj = upscale_backward(src, 1.0, self._adj, out_size=(w, h))
+            if self.upscale_mode == "spline_analytic":
+                adj = PixelAdjoint.from_source(sadj)
+            else:
+                adj = PixelAdjoint.zeros(rw, rh, ds.device)
+                adj.planes[:, :, 0, :] = fd_gradients_backward(sadj)
+            render_backward(ds, fwd, adj, out=self.grads, accumulate=True, check_finite=False)
+        allreduce_grads(self.grads.flat, self.group)
         adam_step(scene_params(ds), grads_dict(self.grads), self.state, self.lrs)
         ds.prepare()   # refresh the view-independent terms for the updated parameters
         return self.values

@@ -86,3 +86,29 @@ def test_training_reduces_loss(P):
     for _ in range(30):
         last = float(tr.step()[0, 0])
     assert last < first
+
+
+def test_bicubic_fd_training_step_matches_oracle(P, oracle):
+    """fit.py's bicubic_fd mode: FD derivative planes, their adjoint folded back (spline.py:291-297)."""
+    import torch
+    from paper_2503_14171_b200 import fit
+    from paper_2503_14171_b200.scenes import synthetic_scene
+    model = synthetic_scene(600, 96, 64, (2.0, 6.0), seed=5)
+    target = np.clip(oracle.render_forward(synthetic_scene(600, 96, 64, (2.0, 6.0), seed=7), 96, 64).color, 0, 1)
+    tr = fit.ViewTrainer(model, (24, 16), (96, 64), [None], [torch.from_numpy(target).float().cuda()],
+                         upscale_mode="bicubic_fd")
+    before = {k: v.clone() for k, v in fit.scene_params(tr.ds).items()}
+    tr.step()
+    got = tr.grads.grads().numpy()
+    fwd = oracle.render_forward(model, 24, 16)
+    src = oracle.fd_gradients(fwd.color)
+    pred = oracle.upscale_spline(*src, 4.0, out_size=(96, 64))
+    _, dpred = oracle.loss(pred, target, 0.2)
+    sadj = oracle.upscale_backward(24, 16, 4.0, dpred, out_size=(96, 64))
+    w = oracle.fd_gradients_backward(*sadj)
+    z = np.zeros_like(w)
+    ref = oracle.render_backward(model, fwd, (w, z, z, z))
+    from test_gpu_backward import rel_err
+    for f in FIELDS:
+        assert rel_err(got[f], ref[f]) < 1e-3, f
+    assert any(not torch.equal(before[k], v) for k, v in fit.scene_params(tr.ds).items())
