@@ -204,14 +204,24 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 // group.  Step k of the blend loop then advances every group by one of ITS
 // candidates (four candidates per warp instruction stream), which roughly
 // halves the lanes idling on candidates that miss their pixels.
-template <bool TRAIN>
 #ifndef RASTER_MIN_BLOCKS
 #define RASTER_MIN_BLOCKS 3
 #endif
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <bool TRAIN>
 __global__ void __launch_bounds__(kBlock, RASTER_MIN_BLOCKS) raster_fwd_kernel(RasterArgs p) {
-    __shared__ PackF s_pack[kWarps][32];
-    __shared__ float4 s_col[kWarps][32];
-    __shared__ uint2 s_id[kWarps][32];   // (rank, list index)
+    // per warp, double-buffered: chunk c+1 is fetched with cp.async (LDGSTS) while chunk c blends
+    __shared__ PackF s_pack[kWarps][2][32];
+    __shared__ float4 s_col[kWarps][2][32];
+    __shared__ uint32_t s_rank[kWarps][2][32];
     __shared__ uint8_t s_list[kWarps][4][32];
 
     const int tile = blockIdx.x;
@@ -232,15 +242,37 @@ __global__ void __launch_bounds__(kBlock, RASTER_MIN_BLOCKS) raster_fwd_kernel(R
     bool active = inside;
     bool flagged = false;
 
-    if (__any_sync(0xffffffffu, active)) {
-        for (uint32_t base = start; base < end; base += 32) {
-            const uint32_t j = base + lane;
-            uint32_t gmask = 0;   // bit q: candidate reaches group q's 4x2 rectangle
-            PackF g;
-            uint32_t r = 0;
-            if (j < end) {
-                r = p.ranks[j];
-                g = p.pack[r];
+    // lane copies its candidate of the chunk at cbase into buffer b
+    auto stage = [&](uint32_t cbase, int b, uint32_t r) {
+        if (cbase + lane < end) {
+            const float4* src = reinterpret_cast<const float4*>(p.pack + r);
+            float4* dst = reinterpret_cast<float4*>(&s_pack[warp][b][lane]);
+            cp_async16(dst, src);
+            cp_async16(dst + 1, src + 1);
+            cp_async16(dst + 2, src + 2);
+            cp_async16(dst + 3, src + 3);
+            cp_async16(&s_col[warp][b][lane], p.sc.color + r);
+            s_rank[warp][b][lane] = r;
+        }
+        cp_async_commit();
+    };
+
+    if (__any_sync(0xffffffffu, active) && start < end) {
+        stage(start, 0, start + lane < end ? p.ranks[start + lane] : 0u);
+        uint32_t r_next = start + 32 + lane < end ? p.ranks[start + 32 + lane] : 0u;
+        int b = 0;
+        for (uint32_t base = start; base < end; base += 32, b ^= 1) {
+            if (base + 32 < end) {
+                stage(base + 32, b ^ 1, r_next);
+                r_next = base + 64 + lane < end ? p.ranks[base + 64 + lane] : 0u;
+            } else {
+                cp_async_commit();   // keep one group per chunk so wait_group 1 means "chunk base landed"
+            }
+            cp_async_wait1();
+            __syncwarp();
+            uint32_t gmask = 0;   // bit g: candidate reaches group g's 4x2 rectangle
+            if (base + lane < end) {
+                const PackF g = s_pack[warp][b][lane];
                 if (ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
                     // groups: the cull ellipse's extent box against each 4x2 rectangle
                     const float lx = g.mxh - g.ex, hx = g.mxh + g.ex;
@@ -252,18 +284,11 @@ __global__ void __launch_bounds__(kBlock, RASTER_MIN_BLOCKS) raster_fwd_kernel(R
                     gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
                 }
             }
-            const uint32_t m = __ballot_sync(0xffffffffu, gmask != 0);
-            const int slot = __popc(m & lt);
-            if (gmask) {
-                s_pack[warp][slot] = g;
-                s_col[warp][slot] = p.sc.color[r];
-                s_id[warp][slot] = make_uint2(r, j);
-            }
             int cnt_my = 0, cnt_max = 0;
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
                 const uint32_t mq = __ballot_sync(0xffffffffu, (gmask >> qq) & 1u);
-                if ((gmask >> qq) & 1u) s_list[warp][qq][__popc(mq & lt)] = (uint8_t)slot;
+                if ((gmask >> qq) & 1u) s_list[warp][qq][__popc(mq & lt)] = (uint8_t)lane;
                 const int c = __popc(mq);
                 cnt_max = max(cnt_max, c);
                 if (qq == q) cnt_my = c;
@@ -272,15 +297,15 @@ __global__ void __launch_bounds__(kBlock, RASTER_MIN_BLOCKS) raster_fwd_kernel(R
             for (int k = 0; k < cnt_max; ++k) {
                 if (active && k < cnt_my) {
                     const int idx = s_list[warp][q][k];
-                    const uint2 id = s_id[warp][idx];
-                    blend_candidate<TRAIN>(p, s_pack[warp][idx], s_col[warp][idx], id.x, id.y, px, py, cx, cy,
-                                           s, active, flagged);
+                    blend_candidate<TRAIN>(p, s_pack[warp][b][idx], s_col[warp][b][idx], s_rank[warp][b][idx],
+                                           base + idx, px, py, cx, cy, s, active, flagged);
                 }
                 if ((k & 7) == 7 && !__any_sync(0xffffffffu, active)) break;
             }
             if (!__any_sync(0xffffffffu, active)) break;
             __syncwarp();
         }
+        cp_async_wait0();
     }
     if (inside) {
         write_pixel<TRAIN>(p, px, py, s);
