@@ -224,94 +224,108 @@ __global__ void __launch_bounds__(kBlock, RASTER_MIN_BLOCKS) raster_fwd_kernel(R
     __shared__ uint32_t s_rank[kWarps][2][32];
     __shared__ uint8_t s_list[kWarps][4][32];
 
-    const int tile = blockIdx.x;
-    const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = lane >> 3, li = lane & 7;
-    const int rx0 = tile_x * kTile + (warp & 1) * 8, ry0 = tile_y * kTile + (warp >> 1) * 4;
-    const int px = rx0 + (q & 1) * 4 + (li & 3), py = ry0 + (q >> 1) * 2 + (li >> 2);
-    const bool inside = px < p.width && py < p.height;
-    const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
-    const float X0 = (float)rx0 + 0.5f, Y0 = (float)ry0 + 0.5f;
-    const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
     const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t nunits = (uint32_t)(p.ntx * ((p.height + kTile - 1) / kTile)) * kWarps;
 
-    Blend<TRAIN> s;
-    s.init();
-    s.last = start;
-    bool active = inside;
-    bool flagged = false;
+    // Persistent, per-warp dynamic scheduling: a warp claims (tile, 8x4 rectangle)
+    // units from a global counter, so neither slow warps of a CTA nor the last wave
+    // leave SM slots idle.  Units are tile-major (neighbouring warps share a tile list
+    // in L2 at about the same time).
+    for (;;) {
+        uint32_t unit = 0;
+        if (lane == 0) unit = atomicAdd(&p.counters[3], 1u);
+        unit = __shfl_sync(0xffffffffu, unit, 0);
+        if (unit >= nunits) break;
+        const int tile = (int)(unit / kWarps), wr = (int)(unit % kWarps);
+        const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
+        const int rx0 = tile_x * kTile + (wr & 1) * 8, ry0 = tile_y * kTile + (wr >> 1) * 4;
+        const int px = rx0 + (q & 1) * 4 + (li & 3), py = ry0 + (q >> 1) * 2 + (li >> 2);
+        const bool inside = px < p.width && py < p.height;
+        const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
+        const float X0 = (float)rx0 + 0.5f, Y0 = (float)ry0 + 0.5f;
+        const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
 
-    // lane copies its candidate of the chunk at cbase into buffer b
-    auto stage = [&](uint32_t cbase, int b, uint32_t r) {
-        if (cbase + lane < end) {
-            const float4* src = reinterpret_cast<const float4*>(p.pack + r);
-            float4* dst = reinterpret_cast<float4*>(&s_pack[warp][b][lane]);
-            cp_async16(dst, src);
-            cp_async16(dst + 1, src + 1);
-            cp_async16(dst + 2, src + 2);
-            cp_async16(dst + 3, src + 3);
-            cp_async16(&s_col[warp][b][lane], p.sc.color + r);
-            s_rank[warp][b][lane] = r;
-        }
-        cp_async_commit();
-    };
+        Blend<TRAIN> s;
+        s.init();
+        s.last = start;
+        bool active = inside;
+        bool flagged = false;
 
-    if (__any_sync(0xffffffffu, active) && start < end) {
-        stage(start, 0, start + lane < end ? p.ranks[start + lane] : 0u);
-        uint32_t r_next = start + 32 + lane < end ? p.ranks[start + 32 + lane] : 0u;
-        int b = 0;
-        for (uint32_t base = start; base < end; base += 32, b ^= 1) {
-            if (base + 32 < end) {
-                stage(base + 32, b ^ 1, r_next);
-                r_next = base + 64 + lane < end ? p.ranks[base + 64 + lane] : 0u;
-            } else {
-                cp_async_commit();   // keep one group per chunk so wait_group 1 means "chunk base landed"
+        // lane copies its candidate of the chunk at cbase into buffer b
+        auto stage = [&](uint32_t cbase, int b, uint32_t r) {
+            if (cbase + lane < end) {
+                const float4* src = reinterpret_cast<const float4*>(p.pack + r);
+                float4* dst = reinterpret_cast<float4*>(&s_pack[warp][b][lane]);
+                cp_async16(dst, src);
+                cp_async16(dst + 1, src + 1);
+                cp_async16(dst + 2, src + 2);
+                cp_async16(dst + 3, src + 3);
+                cp_async16(&s_col[warp][b][lane], p.sc.color + r);
+                s_rank[warp][b][lane] = r;
             }
-            cp_async_wait1();
-            __syncwarp();
-            uint32_t gmask = 0;   // bit g: candidate reaches group g's 4x2 rectangle
-            if (base + lane < end) {
-                const PackF g = s_pack[warp][b][lane];
-                if (ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
-                    // groups: the cull ellipse's extent box against each 4x2 rectangle
-                    const float lx = g.mxh - g.ex, hx = g.mxh + g.ex;
-                    const float ly = g.myh - g.ey, hy = g.myh + g.ey;
-                    const uint32_t c0 = (lx <= X0 + 3.f && hx >= X0) ? 1u : 0u;
-                    const uint32_t c1 = (lx <= X0 + 7.f && hx >= X0 + 4.f) ? 1u : 0u;
-                    const uint32_t r0 = (ly <= Y0 + 1.f && hy >= Y0) ? 1u : 0u;
-                    const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
-                    gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
+            cp_async_commit();
+        };
+
+        if (__any_sync(0xffffffffu, active) && start < end) {
+            stage(start, 0, start + lane < end ? p.ranks[start + lane] : 0u);
+            uint32_t r_next = start + 32 + lane < end ? p.ranks[start + 32 + lane] : 0u;
+            int b = 0;
+            for (uint32_t base = start; base < end; base += 32, b ^= 1) {
+                if (base + 32 < end) {
+                    stage(base + 32, b ^ 1, r_next);
+                    r_next = base + 64 + lane < end ? p.ranks[base + 64 + lane] : 0u;
+                } else {
+                    cp_async_commit();   // one group per chunk: wait_group 1 == "chunk base landed"
                 }
-            }
-            int cnt_my = 0, cnt_max = 0;
+                cp_async_wait1();
+                __syncwarp();
+                uint32_t gmask = 0;   // bit g: candidate reaches group g's 4x2 rectangle
+                if (base + lane < end) {
+                    const PackF g = s_pack[warp][b][lane];
+                    if (ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
+                        // groups: the cull ellipse's extent box against each 4x2 rectangle
+                        const float lx = g.mxh - g.ex, hx = g.mxh + g.ex;
+                        const float ly = g.myh - g.ey, hy = g.myh + g.ey;
+                        const uint32_t c0 = (lx <= X0 + 3.f && hx >= X0) ? 1u : 0u;
+                        const uint32_t c1 = (lx <= X0 + 7.f && hx >= X0 + 4.f) ? 1u : 0u;
+                        const uint32_t r0 = (ly <= Y0 + 1.f && hy >= Y0) ? 1u : 0u;
+                        const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
+                        gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
+                    }
+                }
+                int cnt_my = 0, cnt_max = 0;
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
-                const uint32_t mq = __ballot_sync(0xffffffffu, (gmask >> qq) & 1u);
-                if ((gmask >> qq) & 1u) s_list[warp][qq][__popc(mq & lt)] = (uint8_t)lane;
-                const int c = __popc(mq);
-                cnt_max = max(cnt_max, c);
-                if (qq == q) cnt_my = c;
-            }
-            __syncwarp();
-            for (int k = 0; k < cnt_max; ++k) {
-                if (active && k < cnt_my) {
-                    const int idx = s_list[warp][q][k];
-                    blend_candidate<TRAIN>(p, s_pack[warp][b][idx], s_col[warp][b][idx], s_rank[warp][b][idx],
-                                           base + idx, px, py, cx, cy, s, active, flagged);
+                for (int qq = 0; qq < 4; ++qq) {
+                    const uint32_t mq = __ballot_sync(0xffffffffu, (gmask >> qq) & 1u);
+                    if ((gmask >> qq) & 1u) s_list[warp][qq][__popc(mq & lt)] = (uint8_t)lane;
+                    const int c = __popc(mq);
+                    cnt_max = max(cnt_max, c);
+                    if (qq == q) cnt_my = c;
                 }
-                if ((k & 7) == 7 && !__any_sync(0xffffffffu, active)) break;
+                __syncwarp();
+                for (int k = 0; k < cnt_max; ++k) {
+                    if (active && k < cnt_my) {
+                        const int idx = s_list[warp][q][k];
+                        blend_candidate<TRAIN>(p, s_pack[warp][b][idx], s_col[warp][b][idx],
+                                               s_rank[warp][b][idx], base + idx, px, py, cx, cy, s, active,
+                                               flagged);
+                    }
+                    if ((k & 7) == 7 && !__any_sync(0xffffffffu, active)) break;
+                }
+                if (!__any_sync(0xffffffffu, active)) break;
+                __syncwarp();
             }
-            if (!__any_sync(0xffffffffu, active)) break;
+            cp_async_wait0();
             __syncwarp();
         }
-        cp_async_wait0();
-    }
-    if (inside) {
-        write_pixel<TRAIN>(p, px, py, s);
-        if (flagged) {
-            uint32_t slot = atomicAdd(&p.counters[2], 1u);
-            p.fixup[slot] = (uint32_t)(py * p.width + px);
+        if (inside) {
+            write_pixel<TRAIN>(p, px, py, s);
+            if (flagged) {
+                uint32_t slot = atomicAdd(&p.counters[2], 1u);
+                p.fixup[slot] = (uint32_t)(py * p.width + px);
+            }
         }
     }
 }
@@ -417,12 +431,24 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
     a.state = out.state;
     a.fixup = (uint32_t*)(ws + L.fixup);
     a.counters = (uint32_t*)(ws + L.counters);
-    int ntiles = L.ntx * L.nty;
+    static int grid_inf = 0, grid_train = 0;
+    if (!grid_inf) {
+        int per_sm = 0, dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<false>, kBlock, 0));
+        grid_inf = max(per_sm, 1) * sms;
+        SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<true>, kBlock, 0));
+        grid_train = max(per_sm, 1) * sms;
+    }
+    const int ntiles = L.ntx * L.nty;
+    // counters[2] = fix-up pixels, counters[3] = work-unit cursor of the persistent raster
+    SPLAT_CUDA_CHECK(cudaMemsetAsync(a.counters + 2, 0, 8, stream));
     if (train) {
-        raster_fwd_kernel<true><<<ntiles, kBlock, 0, stream>>>(a); note_launch();
+        raster_fwd_kernel<true><<<min(grid_train, ntiles), kBlock, 0, stream>>>(a); note_launch();
         fixup_kernel<true><<<148 * 4, 256, 0, stream>>>(a); note_launch();
     } else {
-        raster_fwd_kernel<false><<<ntiles, kBlock, 0, stream>>>(a); note_launch();
+        raster_fwd_kernel<false><<<min(grid_inf, ntiles), kBlock, 0, stream>>>(a); note_launch();
         fixup_kernel<false><<<148 * 4, 256, 0, stream>>>(a); note_launch();
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
