@@ -96,6 +96,9 @@ size_t splat_scene_const_bytes(int64_t n);
 size_t splat_scene_workspace_bytes(int64_t n);
 int splat_scene_prepare(const splat_scene_t *scene, void *const_buf, size_t const_bytes,
                         void *workspace, size_t ws_bytes, void *stream);
+/* Recompute the view-independent terms after a parameter update, keeping the
+ * depth order already in const_buf (depths are not optimised, fit.py:163-166). */
+int splat_scene_refresh(const splat_scene_t *scene, void *const_buf, size_t const_bytes, void *stream);
 /* rank -> storage index (int32, n) inside const_buf (sort_by_depth output) */
 const int32_t *splat_scene_order(const void *const_buf, int64_t n);
 

@@ -55,6 +55,7 @@ SIGNATURES = {
     "splat_scene_const_bytes": (SZ, [I64]),
     "splat_scene_workspace_bytes": (SZ, [I64]),
     "splat_scene_prepare": (I32, [ctypes.POINTER(SceneT), P, SZ, P, SZ, P]),
+    "splat_scene_refresh": (I32, [ctypes.POINTER(SceneT), P, SZ, P]),
     "splat_scene_order": (P, [P, I64]),
     "splat_frame_workspace_bytes": (SZ, [I64, I32, I32, I64]),
     "splat_frame_pointers": (I32, [P, I64, I32, I32, I64, ctypes.POINTER(FramePtrsT)]),

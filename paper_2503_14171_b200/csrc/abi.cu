@@ -24,6 +24,7 @@ int set_cuda_error(cudaError_t e, const char* what) {
 
 size_t scene_workspace_bytes_impl(int64_t n);
 int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaStream_t stream);
+int scene_refresh_impl(const splat_scene_t& s, void* const_buf, cudaStream_t stream);
 bool sorted_in_alt(int ntiles);
 int launch_pack64(const SceneConst& sc, const ViewConst& vc, double* out, cudaStream_t stream);
 size_t backward_workspace_bytes_impl(int64_t n, int64_t cap);
@@ -72,6 +73,12 @@ int splat_scene_prepare(const splat_scene_t* scene, void* const_buf, size_t cons
     if (const_bytes < const_layout(scene->n).total || ws_bytes < scene_workspace_bytes_impl(scene->n))
         return set_error(SPLAT_ERR_PARAMETER, "scene buffers too small");
     return scene_prepare_impl(*scene, const_buf, workspace, (cudaStream_t)stream);
+}
+
+int splat_scene_refresh(const splat_scene_t* scene, void* const_buf, size_t const_bytes, void* stream) {
+    if (!scene || scene->n < 0) return set_error(SPLAT_ERR_PARAMETER, "invalid scene");
+    if (const_bytes < const_layout(scene->n).total) return set_error(SPLAT_ERR_PARAMETER, "scene buffer too small");
+    return scene_refresh_impl(*scene, const_buf, (cudaStream_t)stream);
 }
 
 const int32_t* splat_scene_order(const void* const_buf, int64_t n) {

@@ -67,53 +67,81 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict
         s_y[r][c] = yv;
     }
     __syncthreads();
-    // horizontal pass for all halo rows, tile columns
-    for (int e = tid; e < kHalo * kS; e += 256) {
-        const int r = e / kS, c = e - r * kS;
-        double m[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    // horizontal pass, register-blocked: one (row, 4 consecutive columns) item per thread step
+    for (int e = tid; e < kHalo * (kS / 4); e += 256) {
+        const int r = e / (kS / 4), c0 = (e - r * (kS / 4)) * 4;
+        double m[4][5];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const double xv = s_x[r][c + k], yv = s_y[r][c + k], wk = c_wind[k];
-            m[0] = fma(wk, xv, m[0]);
-            m[1] = fma(wk, yv, m[1]);
-            m[2] = fma(wk, xv * xv, m[2]);
-            m[3] = fma(wk, yv * yv, m[3]);
-            m[4] = fma(wk, xv * yv, m[4]);
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) m[i][q] = 0.0;
+#pragma unroll
+        for (int t = 0; t < 14; ++t) {
+            const double xv = s_x[r][c0 + t], yv = s_y[r][c0 + t];
+            const double xx = xv * xv, yy = yv * yv, xy = xv * yv;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int k = t - i;
+                if (k < 0 || k > 10) continue;
+                const double wk = c_wind[k];
+                m[i][0] = fma(wk, xv, m[i][0]);
+                m[i][1] = fma(wk, yv, m[i][1]);
+                m[i][2] = fma(wk, xx, m[i][2]);
+                m[i][3] = fma(wk, yy, m[i][3]);
+                m[i][4] = fma(wk, xy, m[i][4]);
+            }
         }
 #pragma unroll
-        for (int q = 0; q < 5; ++q) s_h[((size_t)q * kHalo + r) * kS + c] = m[q];
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) s_h[((size_t)q * kHalo + r) * kS + c0 + i] = m[i][q];
     }
     __syncthreads();
-    // vertical pass + SSIM map + coefficient maps
-    for (int e = tid; e < kS * kS; e += 256) {
-        const int r = e / kS, c = e - r * kS;
-        const int gy = Y0 + r, gx = X0 + c;
-        if (gy >= h || gx >= w) continue;
-        double m[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    // vertical pass, register-blocked: thread = (column, 4 consecutive rows) -> exactly 256 items
+    {
+        const int c = tid & (kS - 1), r0 = (tid >> 5) * 4;
+        double m[4][5];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const double wk = c_wind[k];
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int q = 0; q < 5; ++q) m[q] = fma(wk, s_h[((size_t)q * kHalo + r + k) * kS + c], m[q]);
+            for (int q = 0; q < 5; ++q) m[i][q] = 0.0;
+#pragma unroll
+        for (int t = 0; t < 14; ++t) {
+            double hv[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) hv[q] = s_h[((size_t)q * kHalo + r0 + t) * kS + c];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int k = t - i;
+                if (k < 0 || k > 10) continue;
+                const double wk = c_wind[k];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) m[i][q] = fma(wk, hv[q], m[i][q]);
+            }
         }
-        const double ux = m[0], uy = m[1];
-        const double sxx = m[2] - ux * ux, syy = m[3] - uy * uy, sxy = m[4] - ux * uy;
-        const double n1 = 2.0 * ux * uy + kC1, n2 = 2.0 * sxy + kC2;
-        const double d1 = ux * ux + uy * uy + kC1, d2 = sxx + syy + kC2;
-        const bool interior = gy >= kR && gy < h - kR && gx >= kR && gx < w - kR;
-        float gux = 0.f, gvx = 0.f, gvxy = 0.f;
-        if (interior) {
-            local += (n1 * n2) / (d1 * d2);
-            const double pq = n1 / d1, qq = n2 / d2;
-            gux = (float)(gscale * (qq * (2.0 * uy * d1 - 2.0 * ux * n1) / (d1 * d1) +
-                                    pq * (-2.0 * uy / d2 + 2.0 * ux * n2 / (d2 * d2))));
-            gvx = (float)(gscale * pq * (-n2 / (d2 * d2)));
-            gvxy = (float)(gscale * pq * (2.0 / d2));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int gy = Y0 + r0 + i, gx = X0 + c;
+            if (gy >= h || gx >= w) continue;
+            const double ux = m[i][0], uy = m[i][1];
+            const double sxx = m[i][2] - ux * ux, syy = m[i][3] - uy * uy, sxy = m[i][4] - ux * uy;
+            const double n1 = 2.0 * ux * uy + kC1, n2 = 2.0 * sxy + kC2;
+            const double d1 = ux * ux + uy * uy + kC1, d2 = sxx + syy + kC2;
+            const bool interior = gy >= kR && gy < h - kR && gx >= kR && gx < w - kR;
+            float gux = 0.f, gvx = 0.f, gvxy = 0.f;
+            if (interior) {
+                local += (n1 * n2) / (d1 * d2);
+                const double pq = n1 / d1, qq = n2 / d2;
+                gux = (float)(gscale * (qq * (2.0 * uy * d1 - 2.0 * ux * n1) / (d1 * d1) +
+                                        pq * (-2.0 * uy / d2 + 2.0 * ux * n2 / (d2 * d2))));
+                gvx = (float)(gscale * pq * (-n2 / (d2 * d2)));
+                gvxy = (float)(gscale * pq * (2.0 / d2));
+            }
+            float* cp = coef + (((size_t)gy * w + gx) * 3 + ch) * 3;
+            cp[0] = gux;
+            cp[1] = gvx;
+            cp[2] = gvxy;
         }
-        float* cp = coef + (((size_t)gy * w + gx) * 3 + ch) * 3;
-        cp[0] = gux;
-        cp[1] = gvx;
-        cp[2] = gvxy;
     }
     // fixed-order block reduction of the SSIM map sum
 #pragma unroll

@@ -327,6 +327,22 @@ int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaSt
     return SPLAT_OK;
 }
 
+// Recompute the view-independent terms for updated parameters, keeping the
+// existing depth order (depths are not optimised: fit.py:163-166).
+int scene_refresh_impl(const splat_scene_t& s, void* const_buf, cudaStream_t stream) {
+    const int64_t n = s.n;
+    if (n == 0) return SPLAT_OK;
+    ConstLayout L = const_layout(n);
+    char* b = (char*)const_buf;
+    scene_const_kernel<<<(int)((n + 255) / 256), 256, 0, stream>>>(
+        n, (const uint32_t*)(b + L.order), s.means, s.log_scales, s.rotations, s.opacity_logits, s.colors,
+        (int32_t*)(b + L.order), (double*)(b + L.mean), (double*)(b + L.n00), (double*)(b + L.n01),
+        (double*)(b + L.n11), (double*)(b + L.e1e2), (double*)(b + L.sigma), (double*)(b + L.q),
+        (float4*)(b + L.color)); note_launch();
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
+
 int launch_preprocess(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
                       cudaStream_t stream) {
     uint32_t* counters = (uint32_t*)(ws + L.counters);

@@ -73,6 +73,15 @@ class DeviceScene:
         self._ws = ws  # keep alive until the stream has consumed it
         return self
 
+    def refresh(self, stream=None) -> "DeviceScene":
+        """Recompute the per-scene terms after an in-place parameter update (same depth order)."""
+        if self.const is None:
+            return self.prepare(stream)
+        lib = _lib.load()
+        _lib.check(lib.splat_scene_refresh(self.c_scene(), _lib.ptr(self.const), self.const.numel(),
+                                           _lib.stream_ptr(stream)))
+        return self
+
     def order(self) -> torch.Tensor:
         """Rank -> storage index (sort_by_depth), int64."""
         lib = _lib.load()

@@ -176,5 +176,5 @@ class ViewTrainer:
             render_backward(ds, fwd, adj, out=self.grads, accumulate=True, check_finite=False)
         allreduce_grads(self.grads.flat, self.group)
         adam_step(scene_params(ds), grads_dict(self.grads), self.state, self.lrs)
-        ds.prepare()   # refresh the view-independent terms for the updated parameters
+        ds.refresh()   # view-independent terms for the updated parameters (depth order is fixed)
         return self.values
