@@ -20,6 +20,7 @@ constexpr double kLogCull = -5.541263545158426;
 struct SceneConst {
     int64_t n;
     const int32_t* order;   // rank -> storage index (stable depth argsort)
+    const int32_t* rank_of; // storage index -> rank (inverse permutation)
     const double* mean;     // (n,2) means gathered into rank order
     const double* n00;      // e1 c^2 + e2 s^2          (raster_forward.py:96)
     const double* n01;      // (e1 - e2) s c            (raster_forward.py:97)

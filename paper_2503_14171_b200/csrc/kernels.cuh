@@ -26,7 +26,7 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap);
 
 // Scene-constant layout inside const_buf.
 struct ConstLayout {
-    size_t order, mean, n00, n01, n11, e1e2, sigma, q, color, total;
+    size_t order, rank_of, mean, n00, n01, n11, e1e2, sigma, q, color, total;
 };
 ConstLayout const_layout(int64_t n);
 SceneConst scene_const_view(const void* buf, int64_t n);

@@ -137,10 +137,11 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict
                 gvx = (float)(gscale * pq * (-n2 / (d2 * d2)));
                 gvxy = (float)(gscale * pq * (2.0 / d2));
             }
-            float* cp = coef + (((size_t)gy * w + gx) * 3 + ch) * 3;
-            cp[0] = gux;
-            cp[1] = gvx;
-            cp[2] = gvxy;
+            // planar coefficient maps [(ch * 3 + q)][H][W]: coalesced stores and loads
+            const size_t hw = (size_t)h * w, o = (size_t)gy * w + gx;
+            coef[(size_t)(ch * 3) * hw + o] = gux;
+            coef[(size_t)(ch * 3 + 1) * hw + o] = gvx;
+            coef[(size_t)(ch * 3 + 2) * hw + o] = gvxy;
         }
     }
     // fixed-order block reduction of the SSIM map sum
@@ -172,10 +173,10 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
         const int gy = Y0 + r - kR, gx = X0 + c - kR;
         float a = 0.f, b = 0.f, d = 0.f;
         if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
-            const float* cp = coef + (((size_t)gy * w + gx) * 3 + ch) * 3;
-            a = cp[0];
-            b = cp[1];
-            d = cp[2];
+            const size_t hw = (size_t)h * w, o = (size_t)gy * w + gx;
+            a = coef[(size_t)(ch * 3) * hw + o];
+            b = coef[(size_t)(ch * 3 + 1) * hw + o];
+            d = coef[(size_t)(ch * 3 + 2) * hw + o];
         }
         s_c[0][r][c] = a;
         s_c[1][r][c] = b;

@@ -39,6 +39,7 @@ __global__ void scene_const_kernel(int64_t n, const uint32_t* __restrict__ order
                                    const double* __restrict__ means, const double* __restrict__ ls,
                                    const double* __restrict__ rot, const double* __restrict__ logit,
                                    const double* __restrict__ colors, int32_t* __restrict__ order_out,
+                                   int32_t* __restrict__ rank_of,
                                    double* __restrict__ mean_r, double* __restrict__ n00,
                                    double* __restrict__ n01, double* __restrict__ n11,
                                    double* __restrict__ e1e2, double* __restrict__ sigma,
@@ -47,6 +48,7 @@ __global__ void scene_const_kernel(int64_t n, const uint32_t* __restrict__ order
     if (r >= n) return;
     int64_t s = order[r];
     order_out[r] = (int32_t)s;
+    rank_of[s] = (int32_t)r;
     mean_r[2 * r] = means[2 * s];
     mean_r[2 * r + 1] = means[2 * s + 1];
     // raster_forward.py:89, 94-98 — same operation order, no contraction
@@ -222,6 +224,7 @@ ConstLayout const_layout(int64_t n) {
     size_t o = 0;
     size_t nn = (size_t)(n > 0 ? n : 1);
     L.order = o; o = align_up(o + nn * 4);
+    L.rank_of = o; o = align_up(o + nn * 4);
     L.mean = o; o = align_up(o + nn * 16);
     L.n00 = o; o = align_up(o + nn * 8);
     L.n01 = o; o = align_up(o + nn * 8);
@@ -240,6 +243,7 @@ SceneConst scene_const_view(const void* buf, int64_t n) {
     SceneConst s;
     s.n = n;
     s.order = (const int32_t*)(b + L.order);
+    s.rank_of = (const int32_t*)(b + L.rank_of);
     s.mean = (const double*)(b + L.mean);
     s.n00 = (const double*)(b + L.n00);
     s.n01 = (const double*)(b + L.n01);
@@ -320,7 +324,8 @@ int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaSt
     char* b = (char*)const_buf;
     scene_const_kernel<<<blocks, 256, 0, stream>>>(
         n, order, s.means, s.log_scales, s.rotations, s.opacity_logits, s.colors,
-        (int32_t*)(b + L.order), (double*)(b + L.mean), (double*)(b + L.n00), (double*)(b + L.n01),
+        (int32_t*)(b + L.order), (int32_t*)(b + L.rank_of), (double*)(b + L.mean), (double*)(b + L.n00),
+        (double*)(b + L.n01),
         (double*)(b + L.n11), (double*)(b + L.e1e2), (double*)(b + L.sigma), (double*)(b + L.q),
         (float4*)(b + L.color)); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
@@ -336,7 +341,8 @@ int scene_refresh_impl(const splat_scene_t& s, void* const_buf, cudaStream_t str
     char* b = (char*)const_buf;
     scene_const_kernel<<<(int)((n + 255) / 256), 256, 0, stream>>>(
         n, (const uint32_t*)(b + L.order), s.means, s.log_scales, s.rotations, s.opacity_logits, s.colors,
-        (int32_t*)(b + L.order), (double*)(b + L.mean), (double*)(b + L.n00), (double*)(b + L.n01),
+        (int32_t*)(b + L.order), (int32_t*)(b + L.rank_of), (double*)(b + L.mean), (double*)(b + L.n00),
+        (double*)(b + L.n01),
         (double*)(b + L.n11), (double*)(b + L.e1e2), (double*)(b + L.sigma), (double*)(b + L.q),
         (float4*)(b + L.color)); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());

@@ -246,37 +246,32 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
     }
 }
 
-// Per splat (rank): sum its pair partials in tile order (raster_backward.py:116-124).
-__global__ void reduce_pairs_kernel(int64_t n, const uint32_t* __restrict__ touched,
-                                    const uint32_t* __restrict__ offsets, const float* __restrict__ partial,
-                                    int64_t cap, float* __restrict__ g9) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    float acc[kG];
+// Per splat, in storage order: sum its (splat, tile) partials in tile order
+// (the reference's fixed tile-order reduction, raster_backward.py:116-124), then
+// chain render-space gradients into the stored parametrisation
+// (raster_backward.py:126-152).  grads layout (float32, n = scene size):
+//   [d_means (n,2) | d_log_scales (n,2) | d_rotations (n) | d_opacity_logits (n) | d_colors (n,3)]
+// Iterating storage order keeps every gradient store coalesced; a splat's
+// partials are contiguous (emission order), read through the inverse order.
+__global__ void reduce_chain_kernel(int64_t n, const int32_t* __restrict__ rank_of,
+                                    const uint32_t* __restrict__ touched, const uint32_t* __restrict__ offsets,
+                                    const float* __restrict__ partial, int64_t cap,
+                                    const double* __restrict__ ls, const double* __restrict__ rot,
+                                    const double* __restrict__ sigma_r, double kx, double ky, int accumulate,
+                                    float* __restrict__ grads) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int64_t r = rank_of[s];
+    float g[kG];
 #pragma unroll
-    for (int i = 0; i < kG; ++i) acc[i] = 0.f;
+    for (int i = 0; i < kG; ++i) g[i] = 0.f;
     const uint32_t off = offsets[r], cnt = touched[r];
     for (uint32_t k = 0; k < cnt; ++k) {
         if ((int64_t)(off + k) >= cap) break;
         const float* src = partial + (size_t)(off + k) * kG;
 #pragma unroll
-        for (int i = 0; i < kG; ++i) acc[i] += src[i];
+        for (int i = 0; i < kG; ++i) g[i] += src[i];
     }
-#pragma unroll
-    for (int i = 0; i < kG; ++i) g9[(size_t)r * kG + i] = acc[i];
-}
-
-// Render-space -> stored parametrisation (raster_backward.py:126-152), scattered
-// back to storage order.  grads layout (float32, n = scene size):
-//   [d_means (n,2) | d_log_scales (n,2) | d_rotations (n) | d_opacity_logits (n) | d_colors (n,3)]
-__global__ void chain_kernel(int64_t n, const int32_t* __restrict__ order, const double* __restrict__ ls,
-                             const double* __restrict__ rot, const double* __restrict__ sigma_r,
-                             const float* __restrict__ g9, double kx, double ky, int accumulate,
-                             float* __restrict__ grads) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const int64_t s = order[r];
-    const float* g = g9 + (size_t)r * kG;
     const double sg = sigma_r[r];
     const double d_sigma = (double)g[3] / sg;
     const double dn00 = (double)g[6] / (2.0 * kx * kx);
@@ -289,15 +284,11 @@ __global__ void chain_kernel(int64_t n, const int32_t* __restrict__ order, const
     const double d_l2 = -2.0 * e2 * (dn00 * sn * sn - dn01 * sn * c + dn11 * c * c);
     const double sin2 = 2.0 * sn * c, cos2 = c * c - sn * sn;
     const double d_rot = (e2 - e1) * sin2 * dn00 + (e1 - e2) * cos2 * dn01 + (e1 - e2) * sin2 * dn11;
-    float* gm = grads;
-    float* gl = grads + 2 * n;
-    float* gr = grads + 4 * n;
-    float* go = grads + 5 * n;
-    float* gc = grads + 6 * n;
     const float v[9] = {(float)((double)g[4] * kx), (float)((double)g[5] * ky), (float)d_l1, (float)d_l2,
-                         (float)d_rot, (float)(d_sigma * sg * (1.0 - sg)), g[0], g[1], g[2]};
-    float* dst[9] = {gm + 2 * s, gm + 2 * s + 1, gl + 2 * s, gl + 2 * s + 1, gr + s, go + s,
-                     gc + 3 * s, gc + 3 * s + 1, gc + 3 * s + 2};
+                        (float)d_rot, (float)(d_sigma * sg * (1.0 - sg)), g[0], g[1], g[2]};
+    float* dst[9] = {grads + 2 * s, grads + 2 * s + 1, grads + 2 * n + 2 * s, grads + 2 * n + 2 * s + 1,
+                     grads + 4 * n + s, grads + 5 * n + s, grads + 6 * n + 3 * s, grads + 6 * n + 3 * s + 1,
+                     grads + 6 * n + 3 * s + 2};
 #pragma unroll
     for (int i = 0; i < 9; ++i) *dst[i] = accumulate ? *dst[i] + v[i] : v[i];
 }
@@ -315,7 +306,6 @@ int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, con
     extern bool sorted_in_alt(int ntiles);
     const size_t nn = (size_t)(L.n > 0 ? L.n : 1), cc = (size_t)(L.cap > 0 ? L.cap : 1);
     float* partial = (float*)bws;
-    float* g9 = (float*)(bws + ((cc * kG * 4 + 255) & ~size_t(255)));
     if (L.n == 0) return SPLAT_OK;
     SPLAT_CUDA_CHECK(cudaMemsetAsync(partial, 0, cc * kG * 4, stream));
     BwdArgs a;
@@ -337,10 +327,10 @@ int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, con
     a.partial = partial;
     raster_bwd_kernel<<<L.ntx * L.nty, kBlock, 0, stream>>>(a); note_launch();
     const int blocks = (int)((L.n + 255) / 256);
-    reduce_pairs_kernel<<<blocks, 256, 0, stream>>>(L.n, (const uint32_t*)(ws + L.touched),
-                                                    (const uint32_t*)(ws + L.offsets), partial, L.cap, g9); note_launch();
-    chain_kernel<<<blocks, 256, 0, stream>>>(L.n, sc.order, scene.log_scales, scene.rotations, sc.sigma, g9,
-                                             vc.kx, vc.ky, accumulate, grads); note_launch();
+    reduce_chain_kernel<<<blocks, 256, 0, stream>>>(L.n, sc.rank_of, (const uint32_t*)(ws + L.touched),
+                                                    (const uint32_t*)(ws + L.offsets), partial, L.cap,
+                                                    scene.log_scales, scene.rotations, sc.sigma, vc.kx, vc.ky,
+                                                    accumulate, grads); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
