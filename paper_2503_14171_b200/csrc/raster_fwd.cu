@@ -157,7 +157,12 @@ __device__ __forceinline__ void write_pixel(const RasterArgs& p, int px, int py,
 }
 
 constexpr float kTermF = 1e-4f;
-constexpr int kWarps = kBlock / 32;
+#ifndef RASTER_THREADS
+#define RASTER_THREADS 128
+#endif
+constexpr int kRasterThreads = RASTER_THREADS;
+constexpr int kWarps = kRasterThreads / 32;   // warps per CTA of the persistent raster
+constexpr int kRects = 8;                     // 8x4 rectangles per 16x16 tile
 
 // One candidate at one pixel: certified decision, blend, termination test.
 template <bool TRAIN>
@@ -205,7 +210,7 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 // candidates (four candidates per warp instruction stream), which roughly
 // halves the lanes idling on candidates that miss their pixels.
 #ifndef RASTER_MIN_BLOCKS
-#define RASTER_MIN_BLOCKS 3
+#define RASTER_MIN_BLOCKS 5
 #endif
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
@@ -217,7 +222,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 template <bool TRAIN>
-__global__ void __launch_bounds__(kBlock, RASTER_MIN_BLOCKS) raster_fwd_kernel(RasterArgs p) {
+__global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_kernel(RasterArgs p) {
     // per warp, double-buffered: chunk c+1 is fetched with cp.async (LDGSTS) while chunk c blends
     __shared__ PackF s_pack[kWarps][2][32];
     __shared__ float4 s_col[kWarps][2][32];
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(kBlock, RASTER_MIN_BLOCKS) raster_fwd_kernel(R
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = lane >> 3, li = lane & 7;
     const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t nunits = (uint32_t)(p.ntx * ((p.height + kTile - 1) / kTile)) * kWarps;
+    const uint32_t nunits = (uint32_t)(p.ntx * ((p.height + kTile - 1) / kTile)) * kRects;
 
     // Persistent, per-warp dynamic scheduling: a warp claims (tile, 8x4 rectangle)
     // units from a global counter, so neither slow warps of a CTA nor the last wave
@@ -238,7 +243,7 @@ __global__ void __launch_bounds__(kBlock, RASTER_MIN_BLOCKS) raster_fwd_kernel(R
         if (lane == 0) unit = atomicAdd(&p.counters[3], 1u);
         unit = __shfl_sync(0xffffffffu, unit, 0);
         if (unit >= nunits) break;
-        const int tile = (int)(unit / kWarps), wr = (int)(unit % kWarps);
+        const int tile = (int)(unit / kRects), wr = (int)(unit % kRects);
         const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
         const int rx0 = tile_x * kTile + (wr & 1) * 8, ry0 = tile_y * kTile + (wr >> 1) * 4;
         const int px = rx0 + (q & 1) * 4 + (li & 3), py = ry0 + (q >> 1) * 2 + (li >> 2);
@@ -436,19 +441,19 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
         int per_sm = 0, dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<false>, kBlock, 0));
+        SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<false>, kRasterThreads, 0));
         grid_inf = max(per_sm, 1) * sms;
-        SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<true>, kBlock, 0));
+        SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<true>, kRasterThreads, 0));
         grid_train = max(per_sm, 1) * sms;
     }
     const int ntiles = L.ntx * L.nty;
     // counters[2] = fix-up pixels, counters[3] = work-unit cursor of the persistent raster
     SPLAT_CUDA_CHECK(cudaMemsetAsync(a.counters + 2, 0, 8, stream));
     if (train) {
-        raster_fwd_kernel<true><<<min(grid_train, ntiles), kBlock, 0, stream>>>(a); note_launch();
+        raster_fwd_kernel<true><<<grid_train, kRasterThreads, 0, stream>>>(a); note_launch();
         fixup_kernel<true><<<148 * 4, 256, 0, stream>>>(a); note_launch();
     } else {
-        raster_fwd_kernel<false><<<min(grid_inf, ntiles), kBlock, 0, stream>>>(a); note_launch();
+        raster_fwd_kernel<false><<<grid_inf, kRasterThreads, 0, stream>>>(a); note_launch();
         fixup_kernel<false><<<148 * 4, 256, 0, stream>>>(a); note_launch();
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
