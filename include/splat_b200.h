@@ -74,11 +74,12 @@ typedef struct {
     int16_t *bboxes;        /* (n,4) x0,x1,y0,y1 half-open, rank order (prepare_scene bboxes) */
     uint32_t *touched;      /* (n) tiles touched per rank, 0 when invalid */
     uint32_t *offsets;      /* (n+1) exclusive scan of touched */
-    uint32_t *keys;         /* (capacity) sorted tile id per pair */
+    uint32_t *keys;         /* (capacity) tile id per pair (only with SPLAT_BIN_KEYS) */
     uint32_t *ranks;        /* (capacity) sorted rank per pair */
     uint32_t *ranges;       /* (ntiles,2) [start,end) into keys/ranks */
-    uint32_t *counters;     /* [0]=pairs [1]=overflow [2]=fix-up pixels; [4]=sticky overflow
-                               (never cleared by the library: the caller zeroes it) */
+    uint32_t *counters;     /* [0]=pairs [1]=overflow [2]=fix-up pixels [3]=raster work cursor;
+                               [4]=sticky overflow (never cleared by the library: the caller
+                               zeroes it); [5]=tiles too long for the shared-memory sort */
     uint32_t *fixup;        /* (H*W) pixels re-rendered by the exact float64 pass */
     float *pack;            /* (n,16) float32 per-view pack */
 } splat_frame_ptrs_t;
@@ -119,8 +120,17 @@ int splat_render_forward(const void *scene_const, int64_t n, const splat_view_t 
 int splat_prepare_view(const void *scene_const, int64_t n, const splat_view_t *view, int width,
                        int height, void *workspace, size_t ws_bytes, int64_t pair_capacity,
                        void *stream);
+/* flags: SPLAT_BIN_OFFSETS also fills `offsets` (rank-major pair slots, needed by
+ * splat_render_backward; splat_render_forward sets it when train != 0);
+ * SPLAT_BIN_KEYS also fills `keys` (the tile id of every pair, for inspection —
+ * the rasterizer only reads `ranges` and `ranks`). */
+#define SPLAT_BIN_OFFSETS 1
+#define SPLAT_BIN_KEYS 2
+/* SPLAT_BIN_ATOMIC forces the binning path used for very large tile grids
+ * (per-pair global atomics + per-tile sort); same output, for testing. */
+#define SPLAT_BIN_ATOMIC 4
 int splat_bin_tiles(int64_t n, int width, int height, void *workspace, size_t ws_bytes,
-                    int64_t pair_capacity, void *stream);
+                    int64_t pair_capacity, int flags, void *stream);
 /* Rasterizer + exact fix-up pass alone, on a frame already prepared and binned
  * by the two calls above (render_forward = prepare_view + bin_tiles + rasterize). */
 int splat_rasterize(const void *scene_const, int64_t n, const splat_view_t *view, int width,

@@ -62,7 +62,7 @@ SIGNATURES = {
     "splat_render_forward": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
                                    ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_prepare_view": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, P, SZ, I64, P]),
-    "splat_bin_tiles": (I32, [I64, I32, I32, P, SZ, I64, P]),
+    "splat_bin_tiles": (I32, [I64, I32, I32, P, SZ, I64, I32, P]),
     "splat_rasterize": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
                               ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_view_pack64": (I32, [P, I64, ctypes.POINTER(ViewT), P, P]),

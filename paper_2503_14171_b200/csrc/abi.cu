@@ -25,7 +25,6 @@ int set_cuda_error(cudaError_t e, const char* what) {
 size_t scene_workspace_bytes_impl(int64_t n);
 int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaStream_t stream);
 int scene_refresh_impl(const splat_scene_t& s, void* const_buf, cudaStream_t stream);
-bool sorted_in_alt(int ntiles);
 int launch_pack64(const SceneConst& sc, const ViewConst& vc, double* out, cudaStream_t stream);
 size_t backward_workspace_bytes_impl(int64_t n, int64_t cap);
 size_t loss_workspace_bytes_impl(int w, int h);
@@ -93,12 +92,11 @@ int splat_frame_pointers(void* workspace, int64_t n, int width, int height, int6
                          splat_frame_ptrs_t* out) {
     FrameLayout L = frame_layout(n, width, height, pair_capacity);
     char* w = (char*)workspace;
-    bool alt = sorted_in_alt(L.ntx * L.nty);
     out->bboxes = (int16_t*)(w + L.bboxes);
     out->touched = (uint32_t*)(w + L.touched);
     out->offsets = (uint32_t*)(w + L.offsets);
-    out->keys = (uint32_t*)(w + (alt ? L.keys1 : L.keys0));
-    out->ranks = (uint32_t*)(w + (alt ? L.vals1 : L.vals0));
+    out->keys = (uint32_t*)(w + L.keys0);
+    out->ranks = (uint32_t*)(w + L.vals0);
     out->ranges = (uint32_t*)(w + L.ranges);
     out->counters = (uint32_t*)(w + L.counters);
     out->fixup = (uint32_t*)(w + L.fixup);
@@ -117,12 +115,12 @@ int splat_prepare_view(const void* scene_const, int64_t n, const splat_view_t* v
 }
 
 int splat_bin_tiles(int64_t n, int width, int height, void* workspace, size_t ws_bytes,
-                    int64_t pair_capacity, void* stream) {
+                    int64_t pair_capacity, int flags, void* stream) {
     int rc = check_dims(width, height);
     if (rc) return rc;
     FrameLayout L = frame_layout(n, width, height, pair_capacity);
     if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
-    return launch_binning(L, (char*)workspace, (cudaStream_t)stream);
+    return launch_binning(L, (char*)workspace, flags, (cudaStream_t)stream);
 }
 
 int splat_view_pack64(const void* scene_const, int64_t n, const splat_view_t* view, double* pack64,
@@ -144,7 +142,7 @@ int splat_render_forward(const void* scene_const, int64_t n, const splat_view_t*
     ViewConst vc = make_view_const(*view);
     char* w = (char*)workspace;
     if ((rc = launch_preprocess(sc, vc, L, w, s))) return rc;
-    if ((rc = launch_binning(L, w, s))) return rc;
+    if ((rc = launch_binning(L, w, train ? SPLAT_BIN_OFFSETS : 0, s))) return rc;
     return launch_raster_forward(sc, vc, L, w, *out, train != 0, s);
 }
 

@@ -10,6 +10,7 @@ int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* s
                        uint32_t* total_out, cudaStream_t stream);
 int64_t radix_blocks(int64_t cap);
 int64_t radix_scratch_words(int64_t cap);
+int radix_passes(int bits);
 template <typename K>
 int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
                      int64_t n_host, int64_t cap, int begin_bit, int end_bit, uint32_t* scratch,
@@ -17,8 +18,8 @@ int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, c
 
 // Frame workspace layout (all offsets 256-byte aligned).
 struct FrameLayout {
-    size_t bboxes, touched, offsets, scan_scratch, keys0, vals0, keys1, vals1, sort_scratch,
-        ranges, counters, fixup, pack, total;
+    size_t bboxes, touched, offsets, scan_scratch, keys0, vals0, vals1, tile_scan,
+        ranges, tile_count, tile_start, cursor, big_list, bin_hist, bin_part, counters, fixup, pack, total;
     int64_t n, cap;
     int width, height, ntx, nty;
 };
@@ -42,7 +43,7 @@ ViewConst make_view_const(const splat_view_t& v);
 
 int launch_preprocess(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
                       cudaStream_t stream);
-int launch_binning(const FrameLayout& L, char* ws, cudaStream_t stream);
+int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t stream);
 int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
                           const splat_gimg_t& out, bool train, cudaStream_t stream);
 

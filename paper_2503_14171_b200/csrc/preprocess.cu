@@ -209,10 +209,394 @@ __global__ void pack64_kernel(SceneConst sc, ViewConst vc, double* __restrict__ 
     o[5] = sc.sigma[r];
 }
 
+// ---- tile binning ------------------------------------------------------------
+// bin_tiles (raster_forward.py:136-149) appends each valid rank, in rank order,
+// to the list of every tile its bbox touches.  Ranks are cut into blocks of
+// kBinBlock consecutive ranks; then
+//   1. count: per block, a tile histogram in shared memory -> row of hist[block][tile]
+//   2. column scan: per tile, exclusive prefix over blocks (two levels:
+//      groups of kColGroup rows, then the group sums) + the tile totals
+//   3. scan of the tile totals -> each list's [start, end)
+//   4. fill: each block counting-sorts its pairs by tile in shared memory,
+//      sorts each (block, tile) run by rank (runs are a few entries long) and
+//      writes it at start[tile] + prefix[block][tile]: lists come out exactly in
+//      the reference's append order, deterministically, without a global sort.
+// Tile grids too large for the shared-memory tables fall back to per-pair
+// global atomics + a per-tile sort (same result).
+
+constexpr int kBinBlock = 4096;      // ranks per block (a histogram row)
+constexpr int kBinThreads = 1024;    // kBinBlock / kBinThreads ranks per thread
+constexpr int kBinRPT = kBinBlock / kBinThreads;
+constexpr int kBinStage = 8192;      // staged pairs per pass of the fill
+constexpr int kColGroup = 16;        // rows per column-scan group
+constexpr int kBinSmemMax = 200 * 1024;
+
+__device__ __forceinline__ void tile_rect(short4 bb, int& tx0, int& tx1, int& ty0, int& ty1) {
+    tx0 = bb.x / kTile;
+    tx1 = (bb.y - 1) / kTile;
+    ty0 = bb.z / kTile;
+    ty1 = (bb.w - 1) / kTile;
+}
+
+__device__ __forceinline__ void write_range(int t, const uint32_t* tile_start, const uint32_t* tile_count,
+                                            uint32_t* ranges, int64_t cap) {
+    const uint32_t st = tile_start[t];
+    ranges[2 * t] = (uint32_t)min((int64_t)st, cap);
+    ranges[2 * t + 1] = (uint32_t)min((int64_t)st + tile_count[t], cap);
+}
+
+__device__ __forceinline__ void put_rank(uint32_t pos, uint32_t r, int64_t cap, uint32_t* ranks, uint32_t* counters) {
+    if ((int64_t)pos < cap) {
+        ranks[pos] = r;
+    } else {
+        atomicOr(&counters[1], 1u);
+        atomicOr(&counters[4], 1u);  // sticky until the caller clears it
+    }
+}
+
+// Tile rectangle of rank r, or an empty one (tx1 < tx0) for untouched ranks.
+struct BinRect {
+    int r, tx0, tx1, ty0, ty1;
+};
+
+__device__ __forceinline__ BinRect bin_rect(int64_t n, int64_t r, const short4* bboxes, const uint32_t* touched) {
+    BinRect q{(int)r, 0, -1, 0, -1};
+    if (r < n) {
+        const uint32_t c = __ldg(touched + r);   // both loads in flight together
+        const short4 bb = __ldg(bboxes + r);
+        if (c != 0) tile_rect(bb, q.tx0, q.tx1, q.ty0, q.ty1);
+    }
+    return q;
+}
+
+__global__ void __launch_bounds__(kBinThreads) count_rows_kernel(int64_t n, const short4* __restrict__ bboxes,
+                                                                 const uint32_t* __restrict__ touched, int ntx,
+                                                                 int ntiles, uint32_t* __restrict__ hist) {
+    extern __shared__ uint32_t h[];
+    const int64_t nblk = (n + kBinBlock - 1) / kBinBlock;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        for (int t = threadIdx.x; t < ntiles; t += blockDim.x) h[t] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kBinRPT; ++j) {
+            const BinRect q = bin_rect(n, blk * kBinBlock + j * kBinThreads + threadIdx.x, bboxes, touched);
+            for (int ty = q.ty0; ty <= q.ty1; ++ty)
+                for (int tx = q.tx0; tx <= q.tx1; ++tx) atomicAdd(&h[ty * ntx + tx], 1u);
+        }
+        __syncthreads();
+        uint32_t* row = hist + (size_t)blk * ntiles;
+        for (int t = threadIdx.x; t < ntiles; t += blockDim.x) row[t] = h[t];
+        __syncthreads();
+    }
+}
+
+// Per (group, tile): exclusive prefix within the group's rows (in place) and the group sum.
+__global__ void colscan_rows_kernel(int ntiles, int nrows, uint32_t* __restrict__ hist, uint32_t* __restrict__ part) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = blockIdx.y;
+    if (t >= ntiles) return;
+    const int r0 = g * kColGroup, nr = min(kColGroup, nrows - r0);
+    uint32_t* col = hist + (size_t)r0 * ntiles + t;
+    uint32_t v[kColGroup];
+#pragma unroll
+    for (int i = 0; i < kColGroup; ++i) v[i] = i < nr ? col[(size_t)i * ntiles] : 0u;   // all loads in flight
+    uint32_t run = 0;
+#pragma unroll
+    for (int i = 0; i < kColGroup; ++i) {
+        if (i < nr) col[(size_t)i * ntiles] = run;
+        run += v[i];
+    }
+    part[(size_t)g * ntiles + t] = run;
+}
+
+// Per tile: exclusive prefix over the group sums (in place) and the tile total.
+__global__ void colscan_groups_kernel(int ntiles, int ngroups, uint32_t* __restrict__ part,
+                                      uint32_t* __restrict__ tile_count, uint32_t* __restrict__ counters) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) counters[5] = 0;
+    if (t >= ntiles) return;
+    uint32_t run = 0;
+    for (int g = 0; g < ngroups; ++g) {
+        const uint32_t v = part[(size_t)g * ntiles + t];
+        part[(size_t)g * ntiles + t] = run;
+        run += v;
+    }
+    tile_count[t] = run;
+}
+
+// In-place exclusive scan of a[0, m) by the whole CTA; returns the total.
+__device__ uint32_t block_exclusive_scan(uint32_t* a, int m, uint32_t* wsum) {
+    const int per = (m + blockDim.x - 1) / blockDim.x;
+    const int i0 = min((int)threadIdx.x * per, m), i1 = min(i0 + per, m);
+    uint32_t local = 0;
+    for (int i = i0; i < i1; ++i) local += a[i];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t inc = local;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        const uint32_t v = lane < nw ? wsum[lane] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += u;
+        }
+        if (lane < nw) wsum[lane] = x - v;   // exclusive warp offsets
+        if (lane == 31) wsum[32] = x;        // total
+    }
+    __syncthreads();
+    uint32_t run = wsum[wid] + inc - local;
+    for (int i = i0; i < i1; ++i) {
+        const uint32_t v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    const uint32_t total = wsum[32];
+    __syncthreads();
+    return total;
+}
+
+__global__ void __launch_bounds__(kBinThreads) fill_rows_kernel(
+    int64_t n, const short4* __restrict__ bboxes, const uint32_t* __restrict__ touched, int ntx, int ntiles,
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ part, const uint32_t* __restrict__ tile_start,
+    const uint32_t* __restrict__ tile_count, uint32_t* __restrict__ ranges, int64_t cap,
+    uint32_t* __restrict__ ranks, uint32_t* __restrict__ keys, uint32_t* __restrict__ counters) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ uint32_t wsum[33];
+    __shared__ int pass_end;
+    uint32_t* loff = smem;                 // per tile: count -> local start -> cursor
+    uint32_t* gbase = smem + ntiles;       // per tile: global slot of this block's run, minus its local start
+    uint32_t* stage = gbase + ntiles;      // staged ranks of the current pass
+    uint16_t* stile = (uint16_t*)(stage + kBinStage);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
+        write_range(t, tile_start, tile_count, ranges, cap);
+    const int64_t nblk = (n + kBinBlock - 1) / kBinBlock;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        BinRect q[kBinRPT];
+#pragma unroll
+        for (int j = 0; j < kBinRPT; ++j)
+            q[j] = bin_rect(n, blk * kBinBlock + j * kBinThreads + threadIdx.x, bboxes, touched);
+        for (int t = threadIdx.x; t < ntiles; t += blockDim.x) loff[t] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kBinRPT; ++j)
+            for (int ty = q[j].ty0; ty <= q[j].ty1; ++ty)
+                for (int tx = q[j].tx0; tx <= q[j].tx1; ++tx) atomicAdd(&loff[ty * ntx + tx], 1u);
+        __syncthreads();
+        const uint32_t* hrow = hist + (size_t)blk * ntiles;
+        const uint32_t* prow = part + (size_t)(blk / kColGroup) * ntiles;
+        const uint32_t total = block_exclusive_scan(loff, ntiles, wsum);
+        for (int t = threadIdx.x; t < ntiles; t += blockDim.x) gbase[t] = tile_start[t] + prow[t] + hrow[t] - loff[t];
+        // passes over tile ranges whose pairs fit the stage (one pass unless the block is dense)
+        int t0 = 0;
+        while (t0 < ntiles) {
+            if (threadIdx.x == 0) {
+                // largest t1 whose tiles [t0, t1) hold <= kBinStage pairs; a single
+                // tile holds <= kBinBlock pairs of a block, so t1 > t0
+                int lo = t0 + 1, hi = ntiles;
+                const uint32_t lim = loff[t0] + kBinStage;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    const uint32_t e = mid < ntiles ? loff[mid] : total;
+                    if (e <= lim) lo = mid;
+                    else hi = mid - 1;
+                }
+                pass_end = lo;
+            }
+            __syncthreads();
+            const int t1 = pass_end;
+            const uint32_t s0 = loff[t0];
+            const uint32_t s1 = t1 < ntiles ? loff[t1] : total;
+            __syncthreads();   // everyone has read loff[t0], loff[t1] before the cursors move
+#pragma unroll
+            for (int j = 0; j < kBinRPT; ++j)
+                for (int ty = q[j].ty0; ty <= q[j].ty1; ++ty) {
+                    const int row = ty * ntx;
+                    for (int tx = q[j].tx0; tx <= q[j].tx1; ++tx) {
+                        const int t = row + tx;
+                        if (t < t0 || t >= t1) continue;
+                        const uint32_t idx = atomicAdd(&loff[t], 1u) - s0;
+                        stage[idx] = (uint32_t)q[j].r;
+                        stile[idx] = (uint16_t)t;
+                    }
+                }
+            __syncthreads();
+            // each (block, tile) run [a, e) is a handful of entries: an entry's place in
+            // its run is the number of smaller ranks in it (ranks are distinct)
+            const int m = (int)(s1 - s0);
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const int t = stile[i];
+                const uint32_t v = stage[i];
+                const int a = t == t0 ? 0 : (int)(loff[t - 1] - s0);
+                const int e = (int)(loff[t] - s0);
+                uint32_t below = 0;
+                for (int j = a; j < e; ++j) below += stage[j] < v;
+                const uint32_t pos = gbase[t] + s0 + (uint32_t)a + below;
+                put_rank(pos, v, cap, ranks, counters);
+                if (keys && (int64_t)pos < cap) keys[pos] = (uint32_t)t;
+            }
+            __syncthreads();
+            t0 = t1;
+        }
+    }
+}
+
+// Fallback for tile grids too large for the shared-memory tables: global atomics.
+__global__ void count_tiles_kernel(int64_t n, const short4* __restrict__ bboxes,
+                                   const uint32_t* __restrict__ touched, int ntx,
+                                   uint32_t* __restrict__ tile_count) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n || touched[r] == 0) return;
+    int tx0, tx1, ty0, ty1;
+    tile_rect(bboxes[r], tx0, tx1, ty0, ty1);
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&tile_count[ty * ntx + tx], 1u);
+}
+
+__global__ void init_ranges_kernel(int ntiles, const uint32_t* __restrict__ tile_start,
+                                   const uint32_t* __restrict__ tile_count, uint32_t* __restrict__ ranges,
+                                   uint32_t* __restrict__ cursor, int64_t cap, uint32_t* __restrict__ counters) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) counters[5] = 0;
+    if (t >= ntiles) return;
+    write_range(t, tile_start, tile_count, ranges, cap);
+    cursor[t] = tile_start[t];
+}
+
+__global__ void fill_tiles_kernel(int64_t n, const short4* __restrict__ bboxes,
+                                  const uint32_t* __restrict__ touched, int ntx, int64_t cap,
+                                  uint32_t* __restrict__ cursor, uint32_t* __restrict__ ranks,
+                                  uint32_t* __restrict__ counters) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n || touched[r] == 0) return;
+    int tx0, tx1, ty0, ty1;
+    tile_rect(bboxes[r], tx0, tx1, ty0, ty1);
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx)
+            put_rank(atomicAdd(&cursor[ty * ntx + tx], 1u), (uint32_t)r, cap, ranks, counters);
+}
+
+constexpr int kSegThreads = 256;
+constexpr int kSegSmall = 8192;      // per-tile lists up to this length: 32 KB smem bitonic, one CTA per tile
+constexpr int kSegThreadsLarge = 1024;
+constexpr int kSegChunk = 32768;     // longer lists: 128 KB chunks sorted in smem, then merged in HBM
+
+__device__ void bitonic_sort_smem(uint32_t* a, int P) {
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint32_t x = a[i], y = a[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((x > y) == up) {
+                        a[i] = y;
+                        a[ixj] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Sort src[0, L) (L <= P_max) through shared memory into dst (may alias src).
+__device__ void sort_run_smem(const uint32_t* src, uint32_t* dst, int L, uint32_t* seg) {
+    int P = 1;
+    while (P < L) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) seg[i] = i < L ? src[i] : 0xffffffffu;
+    __syncthreads();
+    bitonic_sort_smem(seg, P);
+    for (int i = threadIdx.x; i < L; i += blockDim.x) dst[i] = seg[i];
+    __syncthreads();
+}
+
+__device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// One CTA per tile.  Lists longer than kSegSmall are queued for the large kernel.
+__global__ void __launch_bounds__(kSegThreads) segsort_kernel(int ntiles, const uint32_t* __restrict__ ranges,
+                                                              uint32_t* __restrict__ ranks,
+                                                              uint32_t* __restrict__ keys,
+                                                              uint32_t* __restrict__ big_list,
+                                                              uint32_t* __restrict__ counters) {
+    extern __shared__ __align__(16) uint32_t seg[];
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint32_t st = ranges[2 * t], en = ranges[2 * t + 1];
+        const int L = (int)(en - st);
+        if (L == 0) continue;
+        if (L > kSegSmall) {
+            if (threadIdx.x == 0) big_list[atomicAdd(&counters[5], 1u)] = (uint32_t)t;
+            continue;
+        }
+        sort_run_smem(ranks + st, ranks + st, L, seg);
+        if (keys)
+            for (int i = threadIdx.x; i < L; i += blockDim.x) keys[st + i] = (uint32_t)t;
+    }
+}
+
+// Long lists (rare: a tile covered by > kSegSmall splats): one CTA per tile sorts
+// kSegChunk runs in shared memory, then merges runs pairwise in HBM (ranks are
+// unique inside a list, so each element's merged position is its index in its own
+// run plus a lower_bound in the partner run), ping-ponging through `alt`.
+__global__ void __launch_bounds__(kSegThreadsLarge) segsort_large_kernel(const uint32_t* __restrict__ ranges,
+                                                                         uint32_t* __restrict__ ranks,
+                                                                         uint32_t* __restrict__ alt,
+                                                                         uint32_t* __restrict__ keys,
+                                                                         const uint32_t* __restrict__ big_list,
+                                                                         const uint32_t* __restrict__ counters) {
+    extern __shared__ __align__(16) uint32_t seg[];
+    const int nbig = (int)counters[5];
+    for (int w = blockIdx.x; w < nbig; w += gridDim.x) {
+        const int t = (int)big_list[w];
+        const uint32_t st = ranges[2 * t];
+        const int L = (int)(ranges[2 * t + 1] - st);
+        uint32_t* a = ranks + st;
+        uint32_t* b = alt + st;
+        for (int c = 0; c < L; c += kSegChunk) sort_run_smem(a + c, a + c, min(kSegChunk, L - c), seg);
+        for (int run = kSegChunk; run < L; run <<= 1) {
+            for (int i = threadIdx.x; i < L; i += blockDim.x) {
+                const int k = i / run;
+                const int base = (k & ~1) * run;
+                const int pb = (k ^ 1) * run;
+                int pos = i;
+                if (pb < L) {
+                    const int pn = min(run, L - pb);
+                    pos = base + (i - k * run) + lower_bound_u32(a + pb, pn, a[i]);
+                }
+                b[pos] = a[i];
+            }
+            __syncthreads();
+            uint32_t* tmp = a;
+            a = b;
+            b = tmp;
+        }
+        if (a != ranks + st)
+            for (int i = threadIdx.x; i < L; i += blockDim.x) ranks[st + i] = a[i];
+        if (keys)
+            for (int i = threadIdx.x; i < L; i += blockDim.x) keys[st + i] = (uint32_t)t;
+        __syncthreads();
+    }
+}
+
 int tile_key_bits(int ntiles) {
     int bits = 0;
     while ((1 << bits) < ntiles) ++bits;
-    return bits == 0 ? 8 : ((bits + 7) / 8) * 8;
+    return bits == 0 ? 1 : bits;
 }
 
 }  // namespace
@@ -272,10 +656,19 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap) {
     L.scan_scratch = o; o = align_up(o + (size_t)scan_scratch_words(n + 1) * 4);
     L.keys0 = o; o = align_up(o + cc * 4);
     L.vals0 = o; o = align_up(o + cc * 4);
-    L.keys1 = o; o = align_up(o + cc * 4);
-    L.vals1 = o; o = align_up(o + cc * 4);
-    L.sort_scratch = o; o = align_up(o + (size_t)radix_scratch_words(cap) * 4);
+    L.vals1 = o; o = align_up(o + cc * 4);   // merge buffer for very long tile lists
+    L.tile_scan = o; o = align_up(o + (size_t)scan_scratch_words((int64_t)L.ntx * L.nty) * 4);
     L.ranges = o; o = align_up(o + (size_t)L.ntx * L.nty * 8);
+    L.tile_count = o; o = align_up(o + (size_t)L.ntx * L.nty * 4 + 4);
+    L.tile_start = o; o = align_up(o + (size_t)L.ntx * L.nty * 4 + 4);
+    L.cursor = o; o = align_up(o + (size_t)L.ntx * L.nty * 4);
+    {
+        const size_t rows = (size_t)(nn + kBinBlock - 1) / kBinBlock;
+        const size_t groups = (rows + kColGroup - 1) / kColGroup;
+        L.bin_hist = o; o = align_up(o + rows * L.ntx * L.nty * 4);
+        L.bin_part = o; o = align_up(o + groups * L.ntx * L.nty * 4);
+    }
+    L.big_list = o; o = align_up(o + (size_t)L.ntx * L.nty * 4);
     L.counters = o; o = align_up(o + 16 * 4);
     L.fixup = o; o = align_up(o + (size_t)width * height * 4 + 4);
     L.pack = o; o = align_up(o + nn * sizeof(PackF));
@@ -362,29 +755,80 @@ int launch_preprocess(const SceneConst& sc, const ViewConst& vc, const FrameLayo
     return SPLAT_OK;
 }
 
-int launch_binning(const FrameLayout& L, char* ws, cudaStream_t stream) {
+int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t stream) {
+    const bool with_offsets = flags & SPLAT_BIN_OFFSETS;
     uint32_t* counters = (uint32_t*)(ws + L.counters);
     uint32_t* ranges = (uint32_t*)(ws + L.ranges);
-    int ntiles = L.ntx * L.nty;
-    SPLAT_CUDA_CHECK(cudaMemsetAsync(ranges, 0, (size_t)ntiles * 8, stream));
-    if (L.n == 0) return SPLAT_OK;
-    uint32_t* touched = (uint32_t*)(ws + L.touched);
-    uint32_t* offsets = (uint32_t*)(ws + L.offsets);
-    exclusive_scan_u32(touched, offsets, L.n, (uint32_t*)(ws + L.scan_scratch), &counters[0], stream);
-    int blocks = (int)((L.n + 255) / 256);
-    uint32_t* k0 = (uint32_t*)(ws + L.keys0);
-    uint32_t* v0 = (uint32_t*)(ws + L.vals0);
-    uint32_t* k1 = (uint32_t*)(ws + L.keys1);
-    uint32_t* v1 = (uint32_t*)(ws + L.vals1);
-    emit_pairs_kernel<<<blocks, 256, 0, stream>>>(L.n, (const short4*)(ws + L.bboxes), touched,
-                                                  offsets, L.ntx, L.cap, k0, v0, counters); note_launch();
-    int alt = 0;
-    radix_sort_pairs<uint32_t>(k0, v0, k1, v1, counters, 0, L.cap, 0, tile_key_bits(ntiles),
-                               (uint32_t*)(ws + L.sort_scratch), &alt, stream);
-    const uint32_t* keys = alt ? k1 : k0;
-    int rblocks = (int)((L.cap + 255) / 256);
-    if (rblocks > 0)
-        tile_ranges_kernel<<<rblocks, 256, 0, stream>>>(keys, counters, L.cap, ntiles, ranges); note_launch();
+    const int ntiles = L.ntx * L.nty;
+    uint32_t* tile_count = (uint32_t*)(ws + L.tile_count);
+    uint32_t* tile_start = (uint32_t*)(ws + L.tile_start);
+    if (L.n == 0) {
+        SPLAT_CUDA_CHECK(cudaMemsetAsync(ranges, 0, (size_t)ntiles * 8, stream));
+        return SPLAT_OK;
+    }
+    const uint32_t* touched = (const uint32_t*)(ws + L.touched);
+    const short4* bboxes = (const short4*)(ws + L.bboxes);
+    if (with_offsets)   // rank-major pair slots for the backward's partials
+        exclusive_scan_u32(touched, (uint32_t*)(ws + L.offsets), L.n, (uint32_t*)(ws + L.scan_scratch), nullptr,
+                           stream);
+    uint32_t* ranks = (uint32_t*)(ws + L.vals0);
+    uint32_t* keys = (flags & SPLAT_BIN_KEYS) ? (uint32_t*)(ws + L.keys0) : nullptr;
+    uint32_t* scan_tmp = (uint32_t*)(ws + L.tile_scan);
+    const int64_t nrows = (L.n + kBinBlock - 1) / kBinBlock;
+    const int ngroups = (int)((nrows + kColGroup - 1) / kColGroup);
+    const int fill_smem = 8 * ntiles + 6 * kBinStage;
+    const bool staged = ntiles <= 65535 && fill_smem <= kBinSmemMax && L.cap < 0xffffffffLL &&
+                        !(flags & SPLAT_BIN_ATOMIC);
+    if (staged) {
+        static bool configured = false;
+        if (!configured) {
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(count_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kBinSmemMax));
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fill_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kBinSmemMax));
+            configured = true;
+        }
+        uint32_t* hist = (uint32_t*)(ws + L.bin_hist);
+        uint32_t* part = (uint32_t*)(ws + L.bin_part);
+        const int grid = (int)(nrows < 148 * 2 ? nrows : 148 * 2);
+        count_rows_kernel<<<grid, kBinThreads, ntiles * 4, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist);
+        note_launch();
+        colscan_rows_kernel<<<dim3(ceil_div(ntiles, 128), ngroups), 128, 0, stream>>>(ntiles, (int)nrows, hist,
+                                                                                     part);
+        note_launch();
+        colscan_groups_kernel<<<ceil_div(ntiles, 128), 128, 0, stream>>>(ntiles, ngroups, part, tile_count,
+                                                                        counters);
+        note_launch();
+        exclusive_scan_u32(tile_count, tile_start, ntiles, scan_tmp, &counters[0], stream);
+        fill_rows_kernel<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, part,
+                                                                  tile_start, tile_count, ranges, L.cap, ranks,
+                                                                  keys, counters);
+        note_launch();
+        SPLAT_CUDA_CHECK(cudaGetLastError());
+        return SPLAT_OK;
+    } else {
+        const int blocks = (int)((L.n + 255) / 256);
+        SPLAT_CUDA_CHECK(cudaMemsetAsync(tile_count, 0, (size_t)ntiles * 4, stream));
+        count_tiles_kernel<<<blocks, 256, 0, stream>>>(L.n, bboxes, touched, L.ntx, tile_count); note_launch();
+        exclusive_scan_u32(tile_count, tile_start, ntiles, scan_tmp, &counters[0], stream);
+        uint32_t* cursor = (uint32_t*)(ws + L.cursor);
+        init_ranges_kernel<<<ceil_div(ntiles, 256), 256, 0, stream>>>(ntiles, tile_start, tile_count, ranges,
+                                                                      cursor, L.cap, counters); note_launch();
+        fill_tiles_kernel<<<blocks, 256, 0, stream>>>(L.n, bboxes, touched, L.ntx, L.cap, cursor, ranks, counters);
+        note_launch();
+    }
+    static bool configured = false;
+    if (!configured) {
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(segsort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              kSegChunk * 4));
+        configured = true;
+    }
+    uint32_t* big = (uint32_t*)(ws + L.big_list);
+    segsort_kernel<<<ntiles, kSegThreads, kSegSmall * 4, stream>>>(ntiles, ranges, ranks, keys, big, counters);
+    note_launch();
+    segsort_large_kernel<<<148, kSegThreadsLarge, kSegChunk * 4, stream>>>(ranges, ranks, (uint32_t*)(ws + L.vals1),
+                                                                          keys, big, counters);
+    note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
@@ -396,6 +840,6 @@ int launch_pack64(const SceneConst& sc, const ViewConst& vc, double* out, cudaSt
     return SPLAT_OK;
 }
 
-bool sorted_in_alt(int ntiles) { return (tile_key_bits(ntiles) / 8) % 2 == 1; }
+
 
 }  // namespace splat

@@ -303,7 +303,6 @@ size_t backward_workspace_bytes_impl(int64_t n, int64_t cap) {
 int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, const ViewConst& vc,
                            const FrameLayout& L, char* ws, const splat_gimg_t& fwd, const float* adj,
                            char* bws, float* grads, int accumulate, cudaStream_t stream) {
-    extern bool sorted_in_alt(int ntiles);
     const size_t nn = (size_t)(L.n > 0 ? L.n : 1), cc = (size_t)(L.cap > 0 ? L.cap : 1);
     float* partial = (float*)bws;
     if (L.n == 0) return SPLAT_OK;
@@ -315,8 +314,7 @@ int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, con
     a.height = L.height;
     a.ntx = L.ntx;
     a.ranges = (const uint32_t*)(ws + L.ranges);
-    bool alt = sorted_in_alt(L.ntx * L.nty);
-    a.ranks = (const uint32_t*)(ws + (alt ? L.vals1 : L.vals0));
+    a.ranks = (const uint32_t*)(ws + L.vals0);
     a.pack = (const PackF*)(ws + L.pack);
     a.bboxes = (const short4*)(ws + L.bboxes);
     a.offsets = (const uint32_t*)(ws + L.offsets);

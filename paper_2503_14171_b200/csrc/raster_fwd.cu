@@ -424,9 +424,7 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
     a.height = L.height;
     a.ntx = L.ntx;
     a.ranges = (const uint32_t*)(ws + L.ranges);
-    extern bool sorted_in_alt(int ntiles);
-    bool alt = sorted_in_alt(L.ntx * L.nty);
-    a.ranks = (const uint32_t*)(ws + (alt ? L.vals1 : L.vals0));
+    a.ranks = (const uint32_t*)(ws + L.vals0);
     a.pack = (const PackF*)(ws + L.pack);
     a.bboxes = (const short4*)(ws + L.bboxes);
     a.planes = out.planes;

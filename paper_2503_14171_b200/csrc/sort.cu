@@ -109,45 +109,52 @@ __device__ __forceinline__ uint32_t sort_count(const uint32_t* n_dev, int64_t n_
     return (uint32_t)(n < cap ? n : cap);
 }
 
-template <typename K>
+// BITS-wide digits: 8 for multi-pass sorts (64-bit depth keys, >11-bit tile ids),
+// up to 11 so a 2040-tile (960x540) frame's tile ids sort in ONE pass.
+template <typename K, int BITS>
 __global__ void __launch_bounds__(kSortThreads)
 radix_upsweep_kernel(const K* __restrict__ keys, const uint32_t* n_dev, int64_t n_host, int64_t cap,
                      int shift, uint32_t* __restrict__ hist, int nblocks) {
-    __shared__ uint32_t h[256];
-    h[threadIdx.x] = 0;
+    constexpr int D = 1 << BITS;
+    constexpr uint32_t M = D - 1;
+    __shared__ uint32_t h[D];
+    for (int d = threadIdx.x; d < D; d += kSortThreads) h[d] = 0;
     __syncthreads();
     uint32_t n = sort_count(n_dev, n_host, cap);
     int64_t base = (int64_t)blockIdx.x * kSortTile;
     if (base < n) {
         for (int r = 0; r < kSortRounds; ++r) {
             int64_t i = base + r * kSortThreads + threadIdx.x;
-            if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 0xffu], 1u);
+            if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & M], 1u);
         }
     }
     __syncthreads();
-    hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+    for (int d = threadIdx.x; d < D; d += kSortThreads) hist[(int64_t)d * nblocks + blockIdx.x] = h[d];
 }
 
 // Downsweep: warp w of the CTA owns the contiguous sub-chunk
 // [base + w*32*R, base + (w+1)*32*R) and keeps its R items per lane in
 // registers.  Pass 1 counts digits per warp (one __match_any_sync per item,
-// the group leader accumulates into the warp's 256 counters).  The CTA then
+// the group leader accumulates into the warp's counters).  The CTA then
 // derives each item's position in the block-locally sorted order (digit-major,
 // stable) and its digit's global base.  Pass 2 writes items to shared memory at
 // their local position; finally the CTA streams shared memory out, so each
-// digit run is written to global memory with consecutive (coalesced) stores.
-template <typename K>
+// digit run is written to global memory with consecutive stores.
+template <typename K, int BITS>
 __global__ void __launch_bounds__(kSortThreads)
 radix_downsweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                        K* __restrict__ kout, uint32_t* __restrict__ vout,
                        const uint32_t* n_dev, int64_t n_host, int64_t cap, int shift,
                        const uint32_t* __restrict__ hist, int nblocks) {
     constexpr int R = kSortRounds;
+    constexpr int D = 1 << BITS;
+    constexpr uint32_t M = D - 1;
+    constexpr int G = D / kSortThreads;                                         // digits per thread
     extern __shared__ __align__(16) unsigned char sm[];
-    uint32_t(*s_cnt)[256] = reinterpret_cast<uint32_t(*)[256]>(sm);            // [8][256]
-    uint32_t* s_gbase = reinterpret_cast<uint32_t*>(sm + 8 * 256 * 4);           // [256]
-    uint32_t* s_scan = s_gbase + 256;                                          // [33]
-    K* s_k = reinterpret_cast<K*>(sm + 8 * 256 * 4 + 512 * 4);                 // [kSortTile]
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(sm);                          // [8][D]
+    uint32_t* s_gbase = s_cnt + 8 * D;                                          // [D]
+    uint32_t* s_scan = s_gbase + D;                                             // [32]
+    K* s_k = reinterpret_cast<K*>(sm + ((size_t)9 * D + 32) * 4);               // [kSortTile]
     uint32_t* s_v = reinterpret_cast<uint32_t*>(s_k + kSortTile);              // [kSortTile]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t n = sort_count(n_dev, n_host, cap);
@@ -165,31 +172,39 @@ radix_downsweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ v
         k[r] = valid ? kin[i] : K(0);
         v[r] = valid ? vin[i] : 0u;
     }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) s_cnt[warp][lane + 32 * q] = 0;
+    uint32_t* my_cnt = s_cnt + warp * D;
+    for (int d = lane; d < D; d += 32) my_cnt[d] = 0;
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const bool valid = sub + r * 32 + lane < n;
         const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-        const uint32_t d = (uint32_t)(k[r] >> shift) & 0xffu;
+        const uint32_t d = (uint32_t)(k[r] >> shift) & M;
         peers[r] = 0;
         if (valid) {
             peers[r] = __match_any_sync(vmask, d);
-            if ((peers[r] & lt_mask) == 0) s_cnt[warp][d] += __popc(peers[r]);
+            if ((peers[r] & lt_mask) == 0) my_cnt[d] += __popc(peers[r]);
         }
         __syncwarp();
     }
     __syncthreads();
-    // thread t = digit t: warp prefix, block total, block-local digit offset
-    uint32_t tot = 0;
+    // thread t owns digits [t*G, (t+1)*G): warp prefix, block total, block-local offset
+    uint32_t tot[G];
+    uint32_t local = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-        const uint32_t c = s_cnt[w][tid];
-        s_cnt[w][tid] = tot;
-        tot += c;
+    for (int g = 0; g < G; ++g) {
+        const int d = tid * G + g;
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const uint32_t c = s_cnt[w * D + d];
+            s_cnt[w * D + d] = run;
+            run += c;
+        }
+        tot[g] = run;
+        local += run;
     }
-    uint32_t incl = tot;   // inclusive scan of tot over the 256 digits (8 warps x 32)
+    uint32_t incl = local;   // exclusive scan of `local` over the 256 threads
 #pragma unroll
     for (int dd = 1; dd < 32; dd <<= 1) {
         const uint32_t o = __shfl_up_sync(0xffffffffu, incl, dd);
@@ -197,21 +212,25 @@ radix_downsweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ v
     }
     if (lane == 31) s_scan[warp] = incl;
     __syncthreads();
-    uint32_t wpre = 0;
-    for (int w = 0; w < warp; ++w) wpre += s_scan[w];
-    const uint32_t loff = wpre + incl - tot;   // exclusive
+    uint32_t loff = incl - local;
+    for (int w = 0; w < warp; ++w) loff += s_scan[w];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) s_cnt[w][tid] += loff;
-    s_gbase[tid] = hist[(int64_t)tid * nblocks + blockIdx.x] - loff;
+    for (int g = 0; g < G; ++g) {
+        const int d = tid * G + g;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s_cnt[w * D + d] += loff;
+        s_gbase[d] = hist[(int64_t)d * nblocks + blockIdx.x] - loff;
+        loff += tot[g];
+    }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const uint32_t d = (uint32_t)(k[r] >> shift) & 0xffu;
+        const uint32_t d = (uint32_t)(k[r] >> shift) & M;
         uint32_t pos = 0;
-        if (peers[r]) pos = s_cnt[warp][d] + __popc(peers[r] & lt_mask);
+        if (peers[r]) pos = my_cnt[d] + __popc(peers[r] & lt_mask);
         __syncwarp();
         if (peers[r]) {
-            if ((peers[r] & lt_mask) == 0) s_cnt[warp][d] += __popc(peers[r]);
+            if ((peers[r] & lt_mask) == 0) my_cnt[d] += __popc(peers[r]);
             s_k[pos] = k[r];
             s_v[pos] = v[r];
         }
@@ -220,15 +239,15 @@ radix_downsweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ v
     __syncthreads();
     for (int i = tid; i < nblk; i += kSortThreads) {
         const K kk = s_k[i];
-        const uint32_t pos = s_gbase[(uint32_t)(kk >> shift) & 0xffu] + (uint32_t)i;
+        const uint32_t pos = s_gbase[(uint32_t)(kk >> shift) & M] + (uint32_t)i;
         kout[pos] = kk;
         vout[pos] = s_v[i];
     }
 }
 
-template <typename K>
+template <typename K, int BITS>
 constexpr size_t downsweep_smem() {
-    return 8 * 256 * 4 + 512 * 4 + (size_t)kSortTile * (sizeof(K) + 4);
+    return ((size_t)9 * (1 << BITS) + 32) * 4 + (size_t)kSortTile * (sizeof(K) + 4);
 }
 
 }  // namespace
@@ -248,12 +267,36 @@ int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* s
 
 int64_t radix_blocks(int64_t cap) { return (cap + kSortTile - 1) / kSortTile; }
 
+constexpr int kMaxDigits = 2048;   // widest single pass (11 bits)
+
 int64_t radix_scratch_words(int64_t cap) {
     int64_t nb = radix_blocks(cap);
     if (nb == 0) nb = 1;
-    return 256 * nb + 1 + scan_scratch_words(256 * nb + 1);
+    return kMaxDigits * nb + 1 + scan_scratch_words(kMaxDigits * nb + 1);
 }
 
+int radix_passes(int bits) { return bits <= 0 ? 0 : (bits <= 11 ? 1 : (bits + 7) / 8); }
+
+template <typename K, int BITS>
+static int radix_pass(const K* src_k, const uint32_t* src_v, K* dst_k, uint32_t* dst_v, const uint32_t* n_dev,
+                      int64_t n_host, int64_t cap, int shift, uint32_t* hist, uint32_t* hscan, int nb,
+                      cudaStream_t stream) {
+    static bool configured = false;
+    if (!configured) {
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(radix_downsweep_kernel<K, BITS>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)downsweep_smem<K, BITS>()));
+        configured = true;
+    }
+    radix_upsweep_kernel<K, BITS><<<nb, kSortThreads, 0, stream>>>(src_k, n_dev, n_host, cap, shift, hist, nb); note_launch();
+    exclusive_scan_u32(hist, hist, (int64_t)(1 << BITS) * nb, hscan, nullptr, stream);
+    radix_downsweep_kernel<K, BITS><<<nb, kSortThreads, downsweep_smem<K, BITS>(), stream>>>(
+        src_k, src_v, dst_k, dst_v, n_dev, n_host, cap, shift, hist, nb); note_launch();
+    return SPLAT_OK;
+}
+
+// Stable LSD sort of (key, value) on key bits [begin_bit, end_bit): one 11-bit
+// pass when the range fits (tile ids of frames up to 2048 tiles), else 8-bit passes.
 template <typename K>
 int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
                      int64_t n_host, int64_t cap, int begin_bit, int end_bit, uint32_t* scratch,
@@ -261,28 +304,28 @@ int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, c
     int nb = (int)radix_blocks(cap);
     if (nb == 0) nb = 1;
     uint32_t* hist = scratch;
-    uint32_t* hscan = scratch + 256 * (int64_t)nb + 1;
-    static bool configured = false;
-    if (!configured) {
-        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(radix_downsweep_kernel<K>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)downsweep_smem<K>()));
-        configured = true;
-    }
+    uint32_t* hscan = scratch + (int64_t)kMaxDigits * nb + 1;
     K* src_k = keys;
     uint32_t* src_v = vals;
     K* dst_k = keys_alt;
     uint32_t* dst_v = vals_alt;
     int alt = 0;
-    for (int shift = begin_bit; shift < end_bit; shift += 8) {
-        radix_upsweep_kernel<K><<<nb, kSortThreads, 0, stream>>>(src_k, n_dev, n_host, cap, shift,
-                                                                 hist, nb); note_launch();
-        exclusive_scan_u32(hist, hist, 256 * (int64_t)nb, hscan, nullptr, stream);
-        radix_downsweep_kernel<K><<<nb, kSortThreads, downsweep_smem<K>(), stream>>>(src_k, src_v, dst_k, dst_v,
-                                                                   n_dev, n_host, cap, shift, hist, nb); note_launch();
-        K* tk = src_k; src_k = dst_k; dst_k = tk;
-        uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
-        alt ^= 1;
+    const int bits = end_bit - begin_bit;
+    int rc;
+    if (radix_passes(bits) == 1 && bits > 8) {
+        if ((rc = radix_pass<K, 11>(src_k, src_v, dst_k, dst_v, n_dev, n_host, cap, begin_bit, hist, hscan, nb,
+                                    stream)))
+            return rc;
+        alt = 1;
+    } else {
+        for (int shift = begin_bit; shift < end_bit; shift += 8) {
+            if ((rc = radix_pass<K, 8>(src_k, src_v, dst_k, dst_v, n_dev, n_host, cap, shift, hist, hscan, nb,
+                                       stream)))
+                return rc;
+            K* tk = src_k; src_k = dst_k; dst_k = tk;
+            uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
+            alt ^= 1;
+        }
     }
     *result_in_alt = alt;
     return SPLAT_OK;

@@ -69,7 +69,7 @@ class ViewPipeline:
             _lib.check(lib.splat_prepare_view(_lib.ptr(ds.const), ds.n, cv, self.width, self.height,
                                               _lib.ptr(frame.ws), frame.nbytes, frame.capacity, st))
             _lib.check(lib.splat_bin_tiles(ds.n, self.width, self.height, _lib.ptr(frame.ws), frame.nbytes,
-                                           frame.capacity, st))
+                                           frame.capacity, 0, st))
             totals[i] = frame.counters()[0].to(torch.int64)
         return int(int(totals.max()) * margin) + 4096
 
@@ -108,7 +108,7 @@ class ViewPipeline:
             if ev is not None:
                 marks[1].record(slot.stream)
             _lib.check(lib.splat_bin_tiles(ds.n, self.width, self.height, _lib.ptr(fw.ws), fw.nbytes,
-                                           fw.capacity, st))
+                                           fw.capacity, 0, st))
             if ev is not None:
                 marks[2].record(slot.stream)
             _lib.check(lib.splat_rasterize(_lib.ptr(ds.const), ds.n, cv, self.width, self.height, 0,

@@ -29,6 +29,7 @@ __all__ = ["GradientImage", "RenderPack", "TileBins", "Frame", "sort_by_depth", 
            "tile_grid", "bin_tiles", "render_forward", "make_view"]
 
 PLANES = ("color", "d_dx", "d_dy", "d_dxdy")
+BIN_OFFSETS, BIN_KEYS, BIN_ATOMIC = 1, 2, 4   # splat_bin_tiles flags (include/splat_b200.h)
 ALPHAS = ("alpha", "alpha_dx", "alpha_dy", "alpha_dxdy")
 
 
@@ -248,26 +249,28 @@ class TileBins:
         return self.ranks[int(self.offsets[t]):int(self.offsets[t + 1])]
 
 
-def _grow_and_bin(pack: RenderPack, out_w: int, out_h: int, lib, st):
+def _grow_and_bin(pack: RenderPack, out_w: int, out_h: int, lib, st, flags: int = 0):
     frame = pack.frame
     _lib.check(lib.splat_bin_tiles(frame.n, out_w, out_h, _lib.ptr(frame.ws), frame.nbytes,
-                                   frame.capacity, st))
+                                   frame.capacity, BIN_OFFSETS | BIN_KEYS | flags, st))
     cnt = frame.counters()[:2].cpu()
     return int(cnt[0]), bool(cnt[1])
 
 
-def bin_tiles(pack: RenderPack, out_w: int, out_h: int):
-    """(tiles, TileBins) — raster_forward.py:136-149 via emit + device radix sort + ranges."""
+def bin_tiles(pack: RenderPack, out_w: int, out_h: int, *, _flags: int = 0):
+    """(tiles, TileBins) — raster_forward.py:136-149 via per-block tile histograms,
+    a column scan and a stable staged fill (``_flags=BIN_ATOMIC`` selects the
+    large-grid path: per-pair atomics + per-tile sort)."""
     lib = _lib.load()
     st = _lib.stream_ptr()
-    total, overflow = _grow_and_bin(pack, out_w, out_h, lib, st)
+    total, overflow = _grow_and_bin(pack, out_w, out_h, lib, st, _flags)
     if overflow:
         raise RuntimeError("pair capacity exceeded in bin_tiles; re-run prepare_scene")
     frame = pack.frame
     keys, ranks = frame.pairs(total)
     ranges = frame.ranges().to(torch.int64)
     offsets = torch.zeros(frame.ntiles + 1, dtype=torch.int64, device=ranges.device)
-    # empty tiles have start == end == 0; offsets from the per-tile counts
+    # offsets from the per-tile counts
     counts = ranges[:, 1] - ranges[:, 0]
     offsets[1:] = torch.cumsum(counts, 0)
     return tile_grid(out_w, out_h), TileBins(offsets, ranks.to(torch.int64), keys.to(torch.int64))

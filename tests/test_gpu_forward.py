@@ -64,6 +64,45 @@ def test_preprocess_and_binning_bitexact(P, name):
     assert np.array_equal(bins.ranks.cpu().numpy(), g["tile_ranks"])
 
 
+@pytest.mark.parametrize("atomic", [False, True])
+@pytest.mark.parametrize("n", [12000, 70000])
+def test_binning_long_tile_lists(P, oracle, n, atomic):
+    """Dense blocks (several staged fill passes per 1024-rank block) and, on the
+    large-grid path, lists longer than the shared-memory sort (8192) and than
+    several 32768-element chunks (HBM merge passes) stay bit-exact."""
+    from paper_2503_14171_b200.raster_forward import BIN_ATOMIC
+    from paper_2503_14171_b200.scenes import synthetic_scene
+    sc = synthetic_scene(n, 40, 24, (0.3, 6.0), seed=11)
+    w, h = 40, 24
+    pack = P.prepare_scene(sc, w, h)
+    _, bins = P.bin_tiles(pack, w, h, _flags=BIN_ATOMIC if atomic else 0)
+    opack = oracle.prepare_scene(oracle.OScene.of(sc), w, h)
+    off, ranks, keys = oracle.bin_tiles_csr(opack, w, h)
+    assert np.array_equal(bins.offsets.cpu().numpy(), off)
+    assert np.array_equal(bins.ranks.cpu().numpy(), ranks)
+    assert np.array_equal(bins.keys.cpu().numpy(), keys)
+    assert int(np.diff(off).max()) > 8192
+    img = P.render_forward(sc, w, h)
+    ref = oracle.render_forward(sc, w, h)
+    assert_forward_matches(img.numpy(), {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)})
+
+
+def test_binning_paths_agree_at_scale(P):
+    """Config-2 scale (200k splats, 960x540): both binning paths give identical lists."""
+    from paper_2503_14171_b200.raster_forward import BIN_ATOMIC
+    from paper_2503_14171_b200.scenes import CONFIGS, synthetic_scene
+    c = CONFIGS["c2"]
+    sc = synthetic_scene(c.n, c.width, c.height, c.scale_range, seed=5)
+    P.render_forward(sc, c.width, c.height)   # sizes the pair capacity for this scene
+    pack = P.prepare_scene(sc, c.width, c.height)
+    _, a = P.bin_tiles(pack, c.width, c.height)
+    a = [x.cpu().numpy() for x in (a.offsets, a.ranks, a.keys)]
+    _, b = P.bin_tiles(pack, c.width, c.height, _flags=BIN_ATOMIC)
+    b = [x.cpu().numpy() for x in (b.offsets, b.ranks, b.keys)]
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
 @pytest.mark.parametrize("name", golden_names("up_"))
 def test_upscale_matches_reference_golden(P, name):
     g = golden(name)

@@ -31,12 +31,12 @@ for cname in sys.argv[1:] or ["c2", "c3"]:
     st = _lib.stream_ptr()
     def fwd():
         _lib.check(lib.splat_render_forward(_lib.ptr(img.scene.const), img.scene.n, v, c.width, c.height, 0,
-                   img.c_gimg(), _lib.ptr(frame.ws), frame.nbytes, frame.capacity, st))
+                   img.c_gimg(), _lib.ptr(frame.ws), frame.nbytes, frame.capacity, 0, st))
     def prep():
         _lib.check(lib.splat_prepare_view(_lib.ptr(img.scene.const), img.scene.n, v, c.width, c.height,
-                   _lib.ptr(frame.ws), frame.nbytes, frame.capacity, st))
+                   _lib.ptr(frame.ws), frame.nbytes, frame.capacity, 0, st))
     def binning():
-        _lib.check(lib.splat_bin_tiles(img.scene.n, c.width, c.height, _lib.ptr(frame.ws), frame.nbytes, frame.capacity, st))
+        _lib.check(lib.splat_bin_tiles(img.scene.n, c.width, c.height, _lib.ptr(frame.ws), frame.nbytes, frame.capacity, 0, st))
     out = torch.empty((c.out_h, c.out_w, 3), device='cuda')
     def up():
         P.upscale_spline(img, c.factor, out=out)
