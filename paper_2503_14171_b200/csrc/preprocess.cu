@@ -227,7 +227,7 @@ __global__ void pack64_kernel(SceneConst sc, ViewConst vc, double* __restrict__ 
 constexpr int kBinBlock = 4096;      // ranks per block (a histogram row)
 constexpr int kBinThreads = 1024;    // kBinBlock / kBinThreads ranks per thread
 constexpr int kBinRPT = kBinBlock / kBinThreads;
-constexpr int kBinStage = 8192;      // staged pairs per pass of the fill
+constexpr int kBinStage = 16384;     // staged pairs per pass of the fill (2 CTAs/SM fit)
 constexpr int kColGroup = 16;        // rows per column-scan group
 constexpr int kBinSmemMax = 200 * 1024;
 
@@ -363,7 +363,20 @@ __device__ uint32_t block_exclusive_scan(uint32_t* a, int m, uint32_t* wsum) {
     return total;
 }
 
-__global__ void __launch_bounds__(kBinThreads) fill_rows_kernel(
+static_assert(kTile == 16, "tile rectangles below use shifts");
+
+// Packed bbox of rank r, all-zero (an empty tile rectangle) for untouched ranks.
+__device__ __forceinline__ short4 bin_box(int64_t n, int64_t r, const short4* bboxes, const uint32_t* touched) {
+    short4 bb = make_short4(0, 0, 0, 0);
+    if (r < n) {
+        const uint32_t c = __ldg(touched + r);   // both loads in flight together
+        const short4 b = __ldg(bboxes + r);
+        if (c != 0) bb = b;
+    }
+    return bb;
+}
+
+__global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
     int64_t n, const short4* __restrict__ bboxes, const uint32_t* __restrict__ touched, int ntx, int ntiles,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ part, const uint32_t* __restrict__ tile_start,
     const uint32_t* __restrict__ tile_count, uint32_t* __restrict__ ranges, int64_t cap,
@@ -379,16 +392,16 @@ __global__ void __launch_bounds__(kBinThreads) fill_rows_kernel(
         write_range(t, tile_start, tile_count, ranges, cap);
     const int64_t nblk = (n + kBinBlock - 1) / kBinBlock;
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-        BinRect q[kBinRPT];
+        short4 bb[kBinRPT];
 #pragma unroll
         for (int j = 0; j < kBinRPT; ++j)
-            q[j] = bin_rect(n, blk * kBinBlock + j * kBinThreads + threadIdx.x, bboxes, touched);
+            bb[j] = bin_box(n, blk * kBinBlock + j * kBinThreads + threadIdx.x, bboxes, touched);
         for (int t = threadIdx.x; t < ntiles; t += blockDim.x) loff[t] = 0;
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kBinRPT; ++j)
-            for (int ty = q[j].ty0; ty <= q[j].ty1; ++ty)
-                for (int tx = q[j].tx0; tx <= q[j].tx1; ++tx) atomicAdd(&loff[ty * ntx + tx], 1u);
+            for (int ty = bb[j].z >> 4; ty <= (bb[j].w - 1) >> 4; ++ty)
+                for (int tx = bb[j].x >> 4; tx <= (bb[j].y - 1) >> 4; ++tx) atomicAdd(&loff[ty * ntx + tx], 1u);
         __syncthreads();
         const uint32_t* hrow = hist + (size_t)blk * ntiles;
         const uint32_t* prow = part + (size_t)(blk / kColGroup) * ntiles;
@@ -397,7 +410,9 @@ __global__ void __launch_bounds__(kBinThreads) fill_rows_kernel(
         // passes over tile ranges whose pairs fit the stage (one pass unless the block is dense)
         int t0 = 0;
         while (t0 < ntiles) {
-            if (threadIdx.x == 0) {
+            if (total <= kBinStage) {
+                if (threadIdx.x == 0) pass_end = ntiles;
+            } else if (threadIdx.x == 0) {
                 // largest t1 whose tiles [t0, t1) hold <= kBinStage pairs; a single
                 // tile holds <= kBinBlock pairs of a block, so t1 > t0
                 int lo = t0 + 1, hi = ntiles;
@@ -416,17 +431,19 @@ __global__ void __launch_bounds__(kBinThreads) fill_rows_kernel(
             const uint32_t s1 = t1 < ntiles ? loff[t1] : total;
             __syncthreads();   // everyone has read loff[t0], loff[t1] before the cursors move
 #pragma unroll
-            for (int j = 0; j < kBinRPT; ++j)
-                for (int ty = q[j].ty0; ty <= q[j].ty1; ++ty) {
+            for (int j = 0; j < kBinRPT; ++j) {
+                const uint32_t r = (uint32_t)(blk * kBinBlock + j * kBinThreads + threadIdx.x);
+                for (int ty = bb[j].z >> 4; ty <= (bb[j].w - 1) >> 4; ++ty) {
                     const int row = ty * ntx;
-                    for (int tx = q[j].tx0; tx <= q[j].tx1; ++tx) {
+                    for (int tx = bb[j].x >> 4; tx <= (bb[j].y - 1) >> 4; ++tx) {
                         const int t = row + tx;
                         if (t < t0 || t >= t1) continue;
                         const uint32_t idx = atomicAdd(&loff[t], 1u) - s0;
-                        stage[idx] = (uint32_t)q[j].r;
+                        stage[idx] = r;
                         stile[idx] = (uint16_t)t;
                     }
                 }
+            }
             __syncthreads();
             // each (block, tile) run [a, e) is a handful of entries: an entry's place in
             // its run is the number of smaller ranks in it (ranks are distinct)
