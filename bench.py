@@ -27,8 +27,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "upscaled frames/s (4K output, ×4) & output Mpix/s at 1/2/4/8 B200 vs CPU ref"
-WORKLOAD = ("c3: synthetic 1M-Gaussian scene, 960x540 render with analytic gradients, "
-            "x4 gradient-aware spline upscale to 3840x2160, 1024-view batch sharded over ranks")
+WORKLOADS = {
+    "c3": "c3: synthetic 1M-Gaussian scene, 960x540 render with analytic gradients, "
+          "x4 gradient-aware spline upscale to 3840x2160, 1024-view batch sharded over ranks",
+    "c2": "c2: synthetic 200k-Gaussian scene, 960x540 render with analytic gradients, "
+          "x2 gradient-aware spline upscale to 1920x1080",
+    "c4": "c4: synthetic 3M-Gaussian scene, stereo frames of two 1080x1200 eyes (disparity pan), "
+          "x2 gradient-aware spline upscale to 2160x2400 per eye",
+}
 FP32_LANES_PER_SM = 128
 NUM_SMS = 148
 
@@ -39,7 +45,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--views", type=int, default=1024)
+    ap.add_argument("--config", default="c3", choices=["c2", "c3", "c4"],
+                    help="render workload (BASELINE.json configs; c3 is the headline)")
+    ap.add_argument("--views", type=int, default=None, help="views in the batch (default: 1024; c4: 64 frames)")
     ap.add_argument("--slots", type=int, default=4, help="concurrent view streams in the timed region")
     ap.add_argument("--kernel-views", type=int, default=64,
                     help="views of the single-stream per-kernel timing pass (roofline)")
@@ -58,33 +66,58 @@ def dist_env():
     return rank, world, local
 
 
+def metric_of(args):
+    if args.config == "c3":
+        return METRIC
+    c = bench_config(args)
+    what = "stereo frames/s (2 eyes" if args.config == "c4" else "upscaled frames/s ("
+    return f"{what}{', ' if args.config == 'c4' else ''}{c.out_w}x{c.out_h} output, ×{c.factor:g}) at 1 B200 vs CPU ref"
+
+
+def bench_config(args):
+    from paper_2503_14171_b200.scenes import CONFIGS
+    return CONFIGS[args.config]
+
+
+def views_per_frame(args):
+    return 2 if args.config == "c4" else 1
+
+
 def config_dict(args, world, views_per_rank):
-    return {"workload": WORKLOAD, "n_splats": 1_000_000, "render": [960, 540], "output": [3840, 2160],
-            "factor": 4, "views": args.views, "views_per_rank": views_per_rank,
-            "parallelism": f"view-shard x{world}",
-            "l2": "no explicit flush: each view streams ~250 MB (pack, pairs, planes, 99.5 MB output) "
-                  "through the 126 MB L2"}
+    c = bench_config(args)
+    d = {"workload": WORKLOADS[args.config], "n_splats": c.n, "render": [c.width, c.height],
+         "output": [c.out_w, c.out_h], "factor": c.factor, "views": args.views,
+         "views_per_rank": views_per_rank, "parallelism": f"view-shard x{world}",
+         "l2": "no explicit flush: each view streams ~250 MB (pack, pairs, planes, 99.5 MB output) "
+               "through the 126 MB L2" if args.config == "c3" else
+               "no explicit flush: per-view working set (pack, pairs, planes, output) exceeds the 126 MB L2"}
+    if views_per_frame(args) > 1:
+        d["views_per_frame"] = views_per_frame(args)
+    return d
 
 
 # ---------------------------------------------------------------------------
 # CPU reference (oracle port) timing
 # ---------------------------------------------------------------------------
 
-def cpu_reference_view(scene, view):
-    """One C3 view through the CPU oracle (render + x4 upscale); seconds."""
+def cpu_reference_view(scene, view, c):
+    """One view through the CPU oracle (render + upscale); seconds."""
     from oracle import oracle as O
     from paper_2503_14171_b200.scenes import view_scene
     t0 = time.perf_counter()
-    img = O.render_forward(view_scene(scene, view), 960, 540)
-    O.upscale_spline(img.color, img.d_dx, img.d_dy, img.d_dxdy, 4.0)
+    img = O.render_forward(view_scene(scene, view), c.width, c.height)
+    O.upscale_spline(img.color, img.d_dx, img.d_dy, img.d_dxdy, c.factor)
     return time.perf_counter() - t0
 
 
-def make_workload(nviews):
-    from paper_2503_14171_b200.scenes import CONFIGS, random_views, synthetic_scene
-    c = CONFIGS["c3"]
+def make_workload(args):
+    from paper_2503_14171_b200.scenes import random_views, stereo_views, synthetic_scene
+    c = bench_config(args)
     scene = synthetic_scene(c.n, c.width, c.height, c.scale_range, seed=5)
-    views = random_views(nviews, c.width, c.height, seed=11)
+    if args.config == "c4":
+        views = stereo_views(args.views, c.width, c.height, seed=11)
+    else:
+        views = random_views(args.views, c.width, c.height, seed=11)
     return scene, views
 
 
@@ -94,20 +127,22 @@ def run_reference(args):
         return
     from oracle import oracle as O
     O.build()
-    scene, views = make_workload(args.views)
+    c = bench_config(args)
+    scene, views = make_workload(args)
     cores = O.default_threads()
     for i in range(min(args.warmup, 1)):
-        cpu_reference_view(scene, views[i])
-    times = [cpu_reference_view(scene, views[i % len(views)]) for i in range(args.steps)]
+        cpu_reference_view(scene, views[i], c)
+    times = [cpu_reference_view(scene, views[i % len(views)], c) for i in range(args.steps)]
     per_view = sum(times) / len(times)
-    value = 1.0 / per_view
-    sample = f"1 view of the C3 batch per step (views 0..{args.steps - 1}), x1024 extrapolated"
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+    value = 1.0 / (per_view * views_per_frame(args))
+    sample = (f"1 view of the {args.config.upper()} batch per step (views 0..{args.steps - 1}), "
+              f"per-view time x {len(views)} views extrapolated")
+    line = {"impl": "reference", "metric": metric_of(args), "value": value, "unit": "frames/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
             "ms_per_step": per_view * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args, 1, args.views),
-            "mpix_per_s": value * 3840 * 2160 / 1e6,
+            "config": config_dict(args, 1, len(views)),
+            "mpix_per_s": value * views_per_frame(args) * c.out_w * c.out_h / 1e6,
             "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
@@ -285,6 +320,8 @@ def run_train(args):
 
 def main():
     args = parse()
+    if args.views is None:
+        args.views = {"c2": 256, "c3": 1024, "c4": 64}[args.config]
     if args.impl == "reference":
         run_reference(args)
         return
@@ -304,18 +341,23 @@ def main():
     from paper_2503_14171_b200.pipeline import ViewPipeline
 
     lib = _lib.load()
-    scene, views = make_workload(args.views)
-    per = (len(views) + world - 1) // world
+    c = bench_config(args)
+    W, H, F = c.width, c.height, c.factor
+    OW, OH = c.out_w, c.out_h
+    vpf = views_per_frame(args)
+    scene, views = make_workload(args)
+    nframes = len(views) // vpf
+    per = (nframes + world - 1) // world * vpf    # shard whole frames (both eyes on one rank)
     mine = views[rank * per:(rank + 1) * per]
 
-    pipe = ViewPipeline(scene, 960, 540, factor=4.0, slots=args.slots, views_for_capacity=mine)
+    pipe = ViewPipeline(scene, W, H, factor=F, slots=args.slots, views_for_capacity=mine)
 
     # untimed: algorithmic work per view (K = sum contrib_count, E = sum valid bbox areas)
     sample = mine[: min(16, len(mine))]
     from paper_2503_14171_b200.raster_forward import render_forward
     K = E = 0.0
     for v in sample:
-        img = render_forward(pipe.scene, 960, 540, view=v)
+        img = render_forward(pipe.scene, W, H, view=v)
         K += float(img.contrib_count.sum(dtype=torch.int64))
         bb = img.frame.bboxes().to(torch.int64)
         area = (bb[:, 1] - bb[:, 0]) * (bb[:, 3] - bb[:, 2])
@@ -323,9 +365,9 @@ def main():
         del img
     K /= len(sample)
     E /= len(sample)
-    P = 960 * 540
+    P = W * H
     raster_flops = 27.0 * P + 13.0 * E + 69.0 * K
-    up_bytes = 12.0 * 3840 * 2160 + 48.0 * P
+    up_bytes = 12.0 * OW * OH + 48.0 * P
 
     for _ in range(args.warmup):
         pipe.render(mine)
@@ -355,7 +397,7 @@ def main():
     pipe.check()
     # per-kernel timing pass (roofline): the same views on ONE stream with CUDA events
     # around every stage, so each kernel's duration is measured without overlap
-    kpipe = ViewPipeline(pipe.scene, 960, 540, factor=4.0, slots=1, capacity=pipe.capacity)
+    kpipe = ViewPipeline(pipe.scene, W, H, factor=F, slots=1, capacity=pipe.capacity)
     kviews = mine[: max(1, min(args.kernel_views, len(mine)))]
     kpipe.render(kviews)
     torch.cuda.synchronize()
@@ -371,7 +413,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     total_views = per * world if world > 1 else len(mine)
-    value = total_views / (ms_max / 1e3)
+    value = total_views / vpf / (ms_max / 1e3)
 
     # ---- e2e through the public API with host buffers -------------------------------------
     e2e = None
@@ -379,14 +421,14 @@ def main():
         host = {f: torch.from_numpy(np.ascontiguousarray(getattr(scene, f))).pin_memory()
                 for f in ("means", "log_scales", "rotations", "opacity_logits", "colors", "depths")}
         h2d = sum(v.numel() * v.element_size() for v in host.values())
-        ring = [torch.empty((2160, 3840, 3), dtype=torch.float32).pin_memory() for _ in range(4)]
-        d2h = len(mine) * 2160 * 3840 * 3 * 4
+        ring = [torch.empty((OH, OW, 3), dtype=torch.float32).pin_memory() for _ in range(4)]
+        d2h = len(mine) * OH * OW * 3 * 4
 
         def e2e_step():
             dev = {k: v.to("cuda", non_blocking=True) for k, v in host.items()}
             ds = DeviceScene(**dev, background=tuple(scene.background),
                              reference_resolution=tuple(scene.reference_resolution)).prepare()
-            p2 = ViewPipeline(ds, 960, 540, factor=4.0, slots=args.slots, capacity=pipe.capacity)
+            p2 = ViewPipeline(ds, W, H, factor=F, slots=args.slots, capacity=pipe.capacity)
             p2.render(mine, host_out=ring)
             p2.join()
             return p2
@@ -411,7 +453,7 @@ def main():
         et = torch.tensor([max(ems, wall)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": total_views / (float(et.item()) / 1e3), "unit": "frames/s",
+        e2e = {"value": total_views / vpf / (float(et.item()) / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": ksteps, "api": "DeviceScene upload + prepare, ViewPipeline.render(host_out=pinned ring)"}
 
@@ -441,7 +483,7 @@ def main():
                                 "E_bbox_evals_per_view": E, "formula": "27P + 13E + 69K (SURVEY 8d)"},
                 "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (median SM clock in run)"}
         u_ms = stage["upscale"]
-        roof_up = {"kernel": "upscale_x4_kernel", "bound": "hbm",
+        roof_up = {"kernel": "upscale_x4_kernel" if F == 4.0 else "upscale_int_kernel<2>", "bound": "hbm",
                    "measured": f"CUDA events per stage, single-stream pass over {len(kviews)} views",
                    "achieved": up_bytes / (u_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                    "frac": up_bytes / (u_ms * 1e-3) / 1e9 / hbm_peak,
@@ -453,16 +495,17 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         O.build()
-        tcpu = cpu_reference_view(scene, mine[0])
-        cpu = {"value": 1.0 / tcpu, "unit": "frames/s", "cores": O.default_threads(), "kind": "port",
-               "sample": "1 view of the C3 batch through the float64 oracle (render + x4 upscale)"}
+        tcpu = cpu_reference_view(scene, mine[0], c)
+        cpu = {"value": 1.0 / (tcpu * vpf), "unit": "frames/s", "cores": O.default_threads(), "kind": "port",
+               "sample": f"1 view of the {args.config.upper()} batch through the float64 oracle "
+                         f"(render + x{F:g} upscale), x{vpf} views per frame"}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+        line = {"metric": metric_of(args), "value": value, "unit": "frames/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": config_dict(args, world, len(mine)),
-                "mpix_per_s": value * 3840 * 2160 / 1e6,
+                "mpix_per_s": value * vpf * OW * OH / 1e6,
                 "stage_ms_per_view": stage, "gpu_launches": int(launches),
                 "roofline": roof, "roofline_upscale": roof_up, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk}

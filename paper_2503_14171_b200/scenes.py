@@ -80,6 +80,18 @@ def random_views(n_views: int, width: int, height: int, seed: int = 11,
     return out
 
 
+def stereo_views(n_frames: int, width: int, height: int, disparity: float = 3.0, seed: int = 11,
+                 zoom_range=(1.0, 1.25)):
+    """Config 4: per frame a left/right eye pair — one seeded view panned by
+    -/+ disparity/2 reference pixels (SURVEY.md 8(d) "stereo pair = 2 views")."""
+    out = []
+    for v in random_views(n_frames, width, height, seed=seed, zoom_range=zoom_range):
+        ox = min(max(v.ox, disparity / 2), width - width / v.zoom - disparity / 2)
+        out.append(View(v.zoom, ox - disparity / 2, v.oy))
+        out.append(View(v.zoom, ox + disparity / 2, v.oy))
+    return out
+
+
 @dataclass(frozen=True)
 class BenchConfig:
     """BASELINE.json configs, sizes from SURVEY.md 8(d)."""
