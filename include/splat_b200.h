@@ -185,6 +185,19 @@ int splat_fd_gradients(const float *image, int width, int height, float *planes,
 int splat_fd_gradients_backward(const float *dplanes, int width, int height, float *dimage,
                                 float *scratch /* (H,W,3) */, void *stream);
 
+/* ---- wire formats --------------------------------------
+ * GIMG gradient dump body (io.py:100-137 save/load_gradient_dump): 16 planar
+ * float32 (H,W) planes — colour RGB, d_dx RGB, d_dy RGB, d_dxdy RGB, alpha,
+ * alpha_dx, alpha_dy, alpha_dxdy — from / to the device layout (planes
+ * (H,W,4,3), alpha (4,H,W)).  The caller writes / checks the 12-byte header.
+ * unpack zeroes `count` (H,W) when it is non-NULL (a dump has no counts). */
+int splat_gimg_pack(const float *planes, const float *alpha, int width, int height, float *out,
+                    void *stream);
+int splat_gimg_unpack(const float *in, int width, int height, float *planes, float *alpha, int32_t *count,
+                      void *stream);
+/* encode_display (io.py:28-31): clip [0,1], ^(1/2.2), x255, round half even -> uint8. */
+int splat_encode_display(const float *image, int64_t count, uint8_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

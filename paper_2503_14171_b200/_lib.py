@@ -63,6 +63,9 @@ SIGNATURES = {
                                    ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_prepare_view": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, P, SZ, I64, P]),
     "splat_bin_tiles": (I32, [I64, I32, I32, P, SZ, I64, I32, P]),
+    "splat_gimg_pack": (I32, [P, P, I32, I32, P, P]),
+    "splat_gimg_unpack": (I32, [P, I32, I32, P, P, P, P]),
+    "splat_encode_display": (I32, [P, I64, P, P]),
     "splat_rasterize": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
                               ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_view_pack64": (I32, [P, I64, ctypes.POINTER(ViewT), P, P]),

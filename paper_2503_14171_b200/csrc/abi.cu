@@ -44,6 +44,11 @@ int upscale_backward_impl(const float* adj, int out_w, int out_h, float* dsrc, i
 int fd_forward_impl(const float* img, int w, int h, float* planes, cudaStream_t stream);
 int fd_backward_impl(const float* dplanes, int w, int h, float* tmp, float* out, cudaStream_t stream);
 
+int gimg_pack_impl(const float* planes, const float* alpha, int w, int h, float* out, cudaStream_t stream);
+int gimg_unpack_impl(const float* in, int w, int h, float* planes, float* alpha, int32_t* count,
+                     cudaStream_t stream);
+int encode_display_impl(const float* img, int64_t n, uint8_t* out, cudaStream_t stream);
+
 static int check_dims(int width, int height) {
     if (width <= 0 || height <= 0)
         return set_error(SPLAT_ERR_DIMENSION, "output dimensions must be positive");
@@ -238,6 +243,22 @@ int splat_fd_gradients_backward(const float* dplanes, int width, int height, flo
     if (width < 2 || height < 2)
         return set_error(SPLAT_ERR_DIMENSION, "finite differences need at least 2x2 pixels");
     return fd_backward_impl(dplanes, width, height, scratch, dimage, (cudaStream_t)stream);
+}
+
+int splat_gimg_pack(const float* planes, const float* alpha, int width, int height, float* out, void* stream) {
+    if (width <= 0 || height <= 0) return set_error(SPLAT_ERR_DIMENSION, "image dimensions must be positive");
+    return gimg_pack_impl(planes, alpha, width, height, out, (cudaStream_t)stream);
+}
+
+int splat_gimg_unpack(const float* in, int width, int height, float* planes, float* alpha, int32_t* count,
+                      void* stream) {
+    if (width <= 0 || height <= 0) return set_error(SPLAT_ERR_DIMENSION, "image dimensions must be positive");
+    return gimg_unpack_impl(in, width, height, planes, alpha, count, (cudaStream_t)stream);
+}
+
+int splat_encode_display(const float* image, int64_t count, uint8_t* out, void* stream) {
+    if (count < 0) return set_error(SPLAT_ERR_DIMENSION, "negative element count");
+    return encode_display_impl(image, count, out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

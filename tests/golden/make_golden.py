@@ -247,6 +247,30 @@ def train_case():
     save("train_step", **out)
 
 
+def io_case():
+    """Wire formats (reference io.py): scene JSON v1 text, a GIMG dump of a
+    reference render, the reference upscale of the re-loaded dump, and display
+    encoding of values in and beyond [0, 1]."""
+    import tempfile
+    from splinesplat import io as rio
+    sc = _as_ref(sharp_scene(seed=4, n=60, size=40))
+    w, h = 40, 24
+    with tempfile.TemporaryDirectory() as d:
+        rio.save_scene(os.path.join(d, "s.json"), sc)
+        text = open(os.path.join(d, "s.json"), "rb").read()
+        img = rf.render_forward(sc, w, h, threads=8)
+        rio.save_gradient_dump(os.path.join(d, "g.gimg"), img)
+        blob = open(os.path.join(d, "g.gimg"), "rb").read()
+        back = rio.load_gradient_dump(os.path.join(d, "g.gimg"))
+    up = rsp.upscale_spline(back, 2.0)
+    rng = np.random.default_rng(3)
+    enc_in = np.concatenate([rng.uniform(-0.1, 1.1, 4000), np.linspace(0.0, 1.0, 1001),
+                             [0.0, 1.0, -1.0, 2.0]]).astype(np.float32)
+    enc_out = rio.encode_display(enc_in.astype(np.float64))
+    save("io", scene_json=np.frombuffer(text, dtype=np.uint8), gimg=np.frombuffer(blob, dtype=np.uint8),
+         up=up, enc_in=enc_in, enc_out=enc_out, out_w=w, out_h=h, **_scene_arrays(sc))
+
+
 if __name__ == "__main__":
     forward_cases()
     upscale_cases()
@@ -254,3 +278,4 @@ if __name__ == "__main__":
     loss_cases()
     fd_cases()
     train_case()
+    io_case()
