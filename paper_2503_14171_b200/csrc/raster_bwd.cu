@@ -45,13 +45,65 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// Warp reduce-scatter of the nine per-lane gradient terms in 14 shuffles (instead of
+// 9 x 5 butterflies): g[0..7] are halved across lane bits 4, 3, 2 (each lane keeps
+// the half its bit selects and adds the partner's copy of it), then summed across
+// bits 1, 0; g[8] is a plain butterfly.  Returns the sum of term
+// term_of_lane(lane) = 4 b4 + 2 b3 + b2 in every lane; `g8` gets the sum of g[8].
+// The summation order is fixed, so results are deterministic.
+__device__ __forceinline__ float warp_reduce9(const float (&g)[kG], int lane, float& g8) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    float h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float send = b4 ? g[i] : g[i + 4];
+        const float keep = b4 ? g[i + 4] : g[i];
+        h[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    float q[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float send = b3 ? h[i] : h[i + 2];
+        const float keep = b3 ? h[i + 2] : h[i];
+        q[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float v;
+    {
+        const float send = b2 ? q[0] : q[1];
+        const float keep = b2 ? q[1] : q[0];
+        v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    g8 = warp_sum(g[8]);
+    return v;
+}
+
+// Batches of kBwBatch candidates are walked back to front by every warp of the
+// tile independently.  Per-batch, per-warp partials go to one of kRing shared
+// slots; the last warp to finish a batch sums its slot in fixed warp order and
+// writes the (splat, tile) partials, then releases the slot for batch + kRing.
+// Warps thus drift up to kRing batches apart instead of meeting at a block
+// barrier after every batch (their per-batch work differs with coverage).
+constexpr int kRing = 4;
+
+struct BwdShared {
+    PackF pack[kWarps_bw][kBwBatch];
+    float4 col[kWarps_bw][kBwBatch];
+    uint32_t rank[kWarps_bw][kBwBatch];
+    float part[kRing][kWarps_bw][kBwBatch][kG];
+    uint32_t touch[kRing][kWarps_bw];
+    int done[kRing];
+    int epoch[kRing];
+    uint32_t hi[kWarps_bw];
+};
+
 __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
-    __shared__ PackF s_pack[kWarps_bw][kBwBatch];
-    __shared__ float4 s_col[kWarps_bw][kBwBatch];
-    __shared__ uint32_t s_rank[kWarps_bw][kBwBatch];
-    __shared__ float s_part[kWarps_bw][kBwBatch][kG];
-    __shared__ uint32_t s_touch[kWarps_bw];
-    __shared__ uint32_t s_hi[kWarps_bw];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BwdShared& S = *reinterpret_cast<BwdShared*>(smem_raw);
+    auto& s_pack = S.pack;
+    auto& s_col = S.col;
+    auto& s_rank = S.rank;
 
     const int tile = blockIdx.x;
     const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
@@ -97,29 +149,47 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
     // block-wide highest list end among live pixels
     uint32_t hi = live ? my_last : start;
     hi = __reduce_max_sync(0xffffffffu, hi);
-    if (lane == 0) s_hi[warp] = hi;
+    const uint32_t warp_hi = hi;
+    if (lane == 0) S.hi[warp] = hi;
+    if (tid < kRing) {
+        S.done[tid] = 0;
+        S.epoch[tid] = 0;
+    }
     __syncthreads();
     hi = start;
 #pragma unroll
-    for (int k = 0; k < kWarps_bw; ++k) hi = max(hi, s_hi[k]);
+    for (int k = 0; k < kWarps_bw; ++k) hi = max(hi, S.hi[k]);
+    int bi = 0;   // batch index (back to front)
 
-    for (uint32_t top = hi; top > start; top = (top - start > (uint32_t)kBwBatch) ? top - kBwBatch : start) {
+    for (uint32_t top = hi; top > start;
+         top = (top - start > (uint32_t)kBwBatch) ? top - kBwBatch : start, ++bi) {
         const uint32_t lo = (top - start > (uint32_t)kBwBatch) ? top - kBwBatch : start;
         const int nb = (int)(top - lo);
-        // every warp stages the batch and culls it against its own rectangle
+        const int slot = bi % kRing, round = bi / kRing;
+        // this warp stages the batch and culls it against its own rectangle
+        // (skipped when none of its live pixels reaches back this far)
+        const bool work = lo < warp_hi;
         const uint32_t j = lo + lane;
         bool keep = false;
         if (lane < nb) {
             const uint32_t r = p.ranks[j];
-            const PackF g = p.pack[r];
-            keep = ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f);
-            s_pack[warp][lane] = g;
-            s_col[warp][lane] = p.sc.color[r];
             s_rank[warp][lane] = r;
+            if (work) {
+                const PackF g = p.pack[r];
+                keep = ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f);
+                s_pack[warp][lane] = g;
+                s_col[warp][lane] = p.sc.color[r];
+            }
         }
         uint32_t bits = __ballot_sync(0xffffffffu, keep);
         uint32_t touched = 0;
+        // wait until the slot's previous batch has been reduced
+        if (lane == 0)
+            while (*(volatile int*)&S.epoch[slot] != round) {
+            }
         __syncwarp();
+        __threadfence_block();
+        float(*s_part)[kG] = S.part[slot][warp];
         while (bits) {
             const int k = 31 - __clz(bits);   // back to front
             bits &= ~(1u << k);
@@ -143,7 +213,10 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                     const float cc[3] = {col.x, col.y, col.z};
                     // invert the accumulated-alpha state across this splat (float64)
                     const double om = st == kClamped ? (double)1.0e-3f : (double)(1.f - al);
-                    const double inv = 1.0 / om;
+                    // 1/om: float32 reciprocal refined by two float64 Newton steps (|rel err| ~ 1e-16)
+                    double inv = (double)fast_rcp((float)om);
+                    inv = inv * fma(-om, inv, 2.0);
+                    inv = inv * fma(-om, inv, 2.0);
                     const double Tp = T * inv;
                     const double axp = (ax - Tp * (double)gax) * inv;
                     const double ayp = (ay - Tp * (double)gay) * inv;
@@ -206,43 +279,56 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                 }
             }
             if (__any_sync(0xffffffffu, contrib)) {
-#pragma unroll
-                for (int i = 0; i < kG; ++i) gr[i] = warp_sum(gr[i]);
-                if (lane == 0) {
-#pragma unroll
-                    for (int i = 0; i < kG; ++i) s_part[warp][k][i] = gr[i];
-                }
+                float g8;
+                const float v = warp_reduce9(gr, lane, g8);
+                if ((lane & 3) == 0) s_part[k][lane >> 2] = v;   // term 4 b4 + 2 b3 + b2 = lane / 4
+                if (lane == 1) s_part[k][8] = g8;
                 touched |= 1u << k;
             }
         }
-        if (lane == 0) s_touch[warp] = touched;
-        __syncthreads();
-        // fixed warp order: one partial per (splat, tile) pair, written at the pair's
-        // emission slot offsets[r] + (tile index within the splat's tile rectangle)
-        if (tid < nb) {
-            float acc[kG];
+        // publish; the last warp of the batch reduces the slot
+        int prev = 0;
+        if (lane == 0) {
+            S.touch[slot][warp] = touched;
+            __threadfence_block();
+            prev = atomicAdd(&S.done[slot], 1);
+        }
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == kWarps_bw - 1) {
+            __threadfence_block();
+            // fixed warp order: one partial per (splat, tile) pair, written at the pair's
+            // emission slot offsets[r] + (tile index within the splat's tile rectangle)
+            if (lane < nb) {
+                float acc[kG];
 #pragma unroll
-            for (int i = 0; i < kG; ++i) acc[i] = 0.f;
-            bool any = false;
+                for (int i = 0; i < kG; ++i) acc[i] = 0.f;
+                bool any = false;
 #pragma unroll
-            for (int ww = 0; ww < kWarps_bw; ++ww) {
-                if ((s_touch[ww] >> tid) & 1u) {
-                    any = true;
+                for (int ww = 0; ww < kWarps_bw; ++ww) {
+                    if ((*(volatile uint32_t*)&S.touch[slot][ww] >> lane) & 1u) {
+                        any = true;
 #pragma unroll
-                    for (int i = 0; i < kG; ++i) acc[i] += s_part[ww][tid][i];
+                        for (int i = 0; i < kG; ++i) acc[i] += S.part[slot][ww][lane][i];
+                    }
+                }
+                if (any) {
+                    const uint32_t r = s_rank[warp][lane];
+                    const short4 bb = p.bboxes[r];
+                    const int btx0 = bb.x / kTile, bty0 = bb.z / kTile, bnx = (bb.y - 1) / kTile - btx0 + 1;
+                    const uint32_t slot_g = p.offsets[r] + (uint32_t)((tile_y - bty0) * bnx + (tile_x - btx0));
+                    float* dst = p.partial + (size_t)slot_g * kG;
+#pragma unroll
+                    for (int i = 0; i < kG; ++i) dst[i] = acc[i];
                 }
             }
-            if (any) {
-                const uint32_t r = s_rank[0][tid];
-                const short4 bb = p.bboxes[r];
-                const int btx0 = bb.x / kTile, bty0 = bb.z / kTile, bnx = (bb.y - 1) / kTile - btx0 + 1;
-                const uint32_t slot = p.offsets[r] + (uint32_t)((tile_y - bty0) * bnx + (tile_x - btx0));
-                float* dst = p.partial + (size_t)slot * kG;
-#pragma unroll
-                for (int i = 0; i < kG; ++i) dst[i] = acc[i];
+            __syncwarp();
+            if (lane == 0) {
+                S.done[slot] = 0;
+                __threadfence_block();
+                *(volatile int*)&S.epoch[slot] = round + 1;
             }
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
@@ -323,7 +409,13 @@ int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, con
     a.state = fwd.state;
     a.adj = adj;
     a.partial = partial;
-    raster_bwd_kernel<<<L.ntx * L.nty, kBlock, 0, stream>>>(a); note_launch();
+    static bool configured = false;
+    if (!configured) {
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sizeof(BwdShared)));
+        configured = true;
+    }
+    raster_bwd_kernel<<<L.ntx * L.nty, kBlock, sizeof(BwdShared), stream>>>(a); note_launch();
     const int blocks = (int)((L.n + 255) / 256);
     reduce_chain_kernel<<<blocks, 256, 0, stream>>>(L.n, sc.rank_of, (const uint32_t*)(ws + L.touched),
                                                     (const uint32_t*)(ws + L.offsets), partial, L.cap,
