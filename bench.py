@@ -279,6 +279,7 @@ def run_train(args):
     if world > 1:
         dist.barrier()
     launches = lib.splat_kernel_launches() - l0
+    trainer.check()
     ms = D.max_over_ranks(s0.elapsed_time(s1) / args.steps, device="cuda")
     total_views = D.total_items(len(mine), device="cuda")
     value = total_views / (ms / 1e3)

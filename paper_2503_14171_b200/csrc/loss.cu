@@ -40,7 +40,17 @@ __constant__ double c_wind[11];
 // the 1e-3 gradient tolerance.  Inputs and the outputs' consumers stay float32.
 constexpr size_t kStatsSmem = 2 * (size_t)kHalo * (kHalo + 1) * 4 + 5 * (size_t)kHalo * kS * 8;
 
-__global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict__ pred,
+// 1/x for x > 0: float32 reciprocal + two float64 Newton steps (~1 ulp)
+__device__ __forceinline__ double rcp64(double x) {
+    float f;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(f) : "f"((float)x));
+    double r = (double)f;
+    r = r * fma(-x, r, 2.0);
+    r = r * fma(-x, r, 2.0);
+    return r;
+}
+
+__global__ void __launch_bounds__(256, 3) ssim_stats_kernel(const float* __restrict__ pred,
                                                          const float* __restrict__ target, int w, int h,
                                                          double gscale, float* __restrict__ coef,
                                                          double* __restrict__ part_ssim) {
@@ -130,12 +140,13 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict
             const bool interior = gy >= kR && gy < h - kR && gx >= kR && gx < w - kR;
             float gux = 0.f, gvx = 0.f, gvxy = 0.f;
             if (interior) {
-                local += (n1 * n2) / (d1 * d2);
-                const double pq = n1 / d1, qq = n2 / d2;
-                gux = (float)(gscale * (qq * (2.0 * uy * d1 - 2.0 * ux * n1) / (d1 * d1) +
-                                        pq * (-2.0 * uy / d2 + 2.0 * ux * n2 / (d2 * d2))));
-                gvx = (float)(gscale * pq * (-n2 / (d2 * d2)));
-                gvxy = (float)(gscale * pq * (2.0 / d2));
+                const double r1 = rcp64(d1), r2 = rcp64(d2);
+                const double pq = n1 * r1, qq = n2 * r2;
+                local += pq * qq;
+                gux = (float)(gscale * (qq * (2.0 * uy * d1 - 2.0 * ux * n1) * (r1 * r1) +
+                                        pq * (-2.0 * uy * r2 + 2.0 * ux * n2 * (r2 * r2))));
+                gvx = (float)(gscale * pq * (-n2 * (r2 * r2)));
+                gvxy = (float)(gscale * pq * (2.0 * r2));
             }
             // planar coefficient maps [(ch * 3 + q)][H][W]: coalesced stores and loads
             const size_t hw = (size_t)h * w, o = (size_t)gy * w + gx;

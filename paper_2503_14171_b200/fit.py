@@ -156,13 +156,38 @@ class ViewTrainer:
         self.state = AdamState.like(scene_params(self.ds))
         self.values = torch.zeros((max(len(self.views), 1), 2), dtype=torch.float64, device=self.ds.device)
         self._adj = torch.empty((h, w, 3), dtype=torch.float32, device=self.ds.device)
+        self._calibrate()
+
+    def _calibrate(self):
+        """Size the pair buffers once (host-synchronous), with headroom for the
+        scene to evolve; steps then run without any host synchronisation and
+        overflow is caught by :meth:`check` (counters[1] of every frame)."""
+        from .raster_forward import _capacity_hint, _initial_capacity
+        rw, rh = self.render_size
+        need = 0
+        for v in self.views:
+            img = render_forward(self.ds, rw, rh, view=v, train=True)
+            need = max(need, img.stats.get("pairs", 0))
+        key = (self.ds.n, rw, rh)
+        _capacity_hint[key] = max(_initial_capacity(self.ds.n, rw, rh), int(need * 1.5) + 4096)
+        self._frames = []
+
+    def check(self) -> None:
+        """Synchronise and raise if any frame of the last step overflowed its pair buffer."""
+        for f in self._frames:
+            if int(f.counters()[1].item()):
+                self._calibrate()
+                raise RuntimeError("pair capacity exceeded during the training step; buffers were "
+                                   "re-sized, repeat the step")
 
     def step(self) -> torch.Tensor:
         """One step; returns the per-view [loss, ssim] rows (device, no host sync)."""
         ds, (rw, rh), (w, h) = self.ds, self.render_size, self.out_size
         self.grads.zero_()
+        self._frames = []
         for i, (v, tgt) in enumerate(zip(self.views, self.targets)):
-            fwd = render_forward(ds, rw, rh, view=v, train=True)
+            fwd = render_forward(ds, rw, rh, view=v, train=True, sync_check=False)
+            self._frames.append(fwd.frame)
             # fit.py:192-212: the analytic channels, or classical bicubic from FD planes
             src = fwd if self.upscale_mode == "spline_analytic" else fd_gradients(fwd.color)
             pred = upscale_spline(src, 1.0, out_size=(w, h))
