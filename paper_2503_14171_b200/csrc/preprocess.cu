@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
     int64_t n, const short4* __restrict__ bboxes, const uint32_t* __restrict__ touched, int ntx, int ntiles,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ part, const uint32_t* __restrict__ tile_start,
     const uint32_t* __restrict__ tile_count, uint32_t* __restrict__ ranges, int64_t cap,
-    uint32_t* __restrict__ ranks, uint32_t* __restrict__ keys, uint32_t* __restrict__ counters) {
+    uint32_t* __restrict__ ranks, uint32_t* __restrict__ keys, uint32_t* __restrict__ counters,
+    const uint32_t* __restrict__ offsets, uint32_t* __restrict__ slot_pos) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t wsum[33];
     __shared__ int pass_end;
@@ -458,10 +459,34 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
                 const uint32_t pos = gbase[t] + s0 + (uint32_t)a + below;
                 put_rank(pos, v, cap, ranks, counters);
                 if (keys && (int64_t)pos < cap) keys[pos] = (uint32_t)t;
+                if (slot_pos) {   // training: emission slot -> list position (see slot_map_kernel)
+                    const short4 b = bboxes[v];
+                    const int tx0 = b.x >> 4, ty0 = b.z >> 4, nx = ((b.y - 1) >> 4) - tx0 + 1;
+                    const int64_t e = (int64_t)offsets[v] + (t / ntx - ty0) * nx + (t % ntx - tx0);
+                    if (e < cap) slot_pos[e] = pos;
+                }
             }
             __syncthreads();
             t0 = t1;
         }
+    }
+}
+
+// Training mode: list position of every pair, indexed by its emission slot
+// offsets[r] + (tile index inside r's tile rectangle) — the backward writes
+// per-pair partials at list positions and reduces them per rank through this map.
+__global__ void slot_map_kernel(int ntx, const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ ranks,
+                                const short4* __restrict__ bboxes, const uint32_t* __restrict__ offsets,
+                                int64_t cap, uint32_t* __restrict__ slot_pos) {
+    const int t = blockIdx.x;
+    const int tx = t % ntx, ty = t / ntx;
+    const uint32_t st = ranges[2 * t], en = ranges[2 * t + 1];
+    for (uint32_t j = st + threadIdx.x; j < en; j += blockDim.x) {
+        const uint32_t r = ranks[j];
+        const short4 bb = bboxes[r];
+        const int tx0 = bb.x >> 4, ty0 = bb.z >> 4, nx = ((bb.y - 1) >> 4) - tx0 + 1;
+        const int64_t e = (int64_t)offsets[r] + (ty - ty0) * nx + (tx - tx0);
+        if (e < cap) slot_pos[e] = j;
     }
 }
 
@@ -674,6 +699,7 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap) {
     L.keys0 = o; o = align_up(o + cc * 4);
     L.vals0 = o; o = align_up(o + cc * 4);
     L.vals1 = o; o = align_up(o + cc * 4);   // merge buffer for very long tile lists
+    L.slot_pos = o; o = align_up(o + cc * 4);   // training: list position of each emission slot
     L.tile_scan = o; o = align_up(o + (size_t)scan_scratch_words((int64_t)L.ntx * L.nty) * 4);
     L.ranges = o; o = align_up(o + (size_t)L.ntx * L.nty * 8);
     L.tile_count = o; o = align_up(o + (size_t)L.ntx * L.nty * 4 + 4);
@@ -819,7 +845,8 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         exclusive_scan_u32(tile_count, tile_start, ntiles, scan_tmp, &counters[0], stream);
         fill_rows_kernel<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, part,
                                                                   tile_start, tile_count, ranges, L.cap, ranks,
-                                                                  keys, counters);
+                                                                  keys, counters, (const uint32_t*)(ws + L.offsets),
+                                                                  with_offsets ? (uint32_t*)(ws + L.slot_pos) : nullptr);
         note_launch();
         SPLAT_CUDA_CHECK(cudaGetLastError());
         return SPLAT_OK;
@@ -846,6 +873,11 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
     segsort_large_kernel<<<148, kSegThreadsLarge, kSegChunk * 4, stream>>>(ranges, ranks, (uint32_t*)(ws + L.vals1),
                                                                           keys, big, counters);
     note_launch();
+    if (with_offsets) {
+        slot_map_kernel<<<ntiles, 256, 0, stream>>>(L.ntx, ranges, ranks, bboxes, (const uint32_t*)(ws + L.offsets),
+                                                    L.cap, (uint32_t*)(ws + L.slot_pos));
+        note_launch();
+    }
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }

@@ -160,6 +160,11 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
 #pragma unroll
     for (int k = 0; k < kWarps_bw; ++k) hi = max(hi, S.hi[k]);
     int bi = 0;   // batch index (back to front)
+    // pairs no live pixel reaches back to get zero partials: every pair of the
+    // tile list is written exactly once (at its list position, so this tile's
+    // partials are one contiguous run) and the buffer needs no clearing
+    for (uint32_t e = (hi - start) * kG + tid; e < (end - start) * kG; e += kBlock)
+        p.partial[(size_t)start * kG + e] = 0.f;
 
     for (uint32_t top = hi; top > start;
          top = (top - start > (uint32_t)kBwBatch) ? top - kBwBatch : start, ++bi) {
@@ -296,27 +301,20 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
         prev = __shfl_sync(0xffffffffu, prev, 0);
         if (prev == kWarps_bw - 1) {
             __threadfence_block();
-            // fixed warp order: one partial per (splat, tile) pair, written at the pair's
-            // emission slot offsets[r] + (tile index within the splat's tile rectangle)
+            // fixed warp order: one partial per (splat, tile) pair, at its list position
             if (lane < nb) {
                 float acc[kG];
 #pragma unroll
                 for (int i = 0; i < kG; ++i) acc[i] = 0.f;
-                bool any = false;
 #pragma unroll
                 for (int ww = 0; ww < kWarps_bw; ++ww) {
                     if ((*(volatile uint32_t*)&S.touch[slot][ww] >> lane) & 1u) {
-                        any = true;
 #pragma unroll
                         for (int i = 0; i < kG; ++i) acc[i] += S.part[slot][ww][lane][i];
                     }
                 }
-                if (any) {
-                    const uint32_t r = s_rank[warp][lane];
-                    const short4 bb = p.bboxes[r];
-                    const int btx0 = bb.x / kTile, bty0 = bb.z / kTile, bnx = (bb.y - 1) / kTile - btx0 + 1;
-                    const uint32_t slot_g = p.offsets[r] + (uint32_t)((tile_y - bty0) * bnx + (tile_x - btx0));
-                    float* dst = p.partial + (size_t)slot_g * kG;
+                {
+                    float* dst = p.partial + (size_t)(lo + lane) * kG;
 #pragma unroll
                     for (int i = 0; i < kG; ++i) dst[i] = acc[i];
                 }
@@ -332,32 +330,43 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
     }
 }
 
-// Per splat, in storage order: sum its (splat, tile) partials in tile order
-// (the reference's fixed tile-order reduction, raster_backward.py:116-124), then
-// chain render-space gradients into the stored parametrisation
-// (raster_backward.py:126-152).  grads layout (float32, n = scene size):
-//   [d_means (n,2) | d_log_scales (n,2) | d_rotations (n) | d_opacity_logits (n) | d_colors (n,3)]
-// Iterating storage order keeps every gradient store coalesced; a splat's
-// partials are contiguous (emission order), read through the inverse order.
-__global__ void reduce_chain_kernel(int64_t n, const int32_t* __restrict__ rank_of,
-                                    const uint32_t* __restrict__ touched, const uint32_t* __restrict__ offsets,
-                                    const float* __restrict__ partial, int64_t cap,
-                                    const double* __restrict__ ls, const double* __restrict__ rot,
-                                    const double* __restrict__ sigma_r, double kx, double ky, int accumulate,
-                                    float* __restrict__ grads) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    const int64_t r = rank_of[s];
+// Per rank: sum its (splat, tile) partials in tile order, the reference's fixed
+// tile-order reduction (raster_backward.py:116-124).  The rank's pairs are the
+// emission slots offsets[r] .. + touched[r] (tile-rectangle order); slot_pos
+// maps each to its list position, where the backward left the partial.
+__global__ void reduce_pairs_kernel(int64_t n, const uint32_t* __restrict__ touched,
+                                    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ slot_pos,
+                                    const float* __restrict__ partial, int64_t cap, float* __restrict__ g_rank) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
     float g[kG];
 #pragma unroll
     for (int i = 0; i < kG; ++i) g[i] = 0.f;
     const uint32_t off = offsets[r], cnt = touched[r];
     for (uint32_t k = 0; k < cnt; ++k) {
         if ((int64_t)(off + k) >= cap) break;
-        const float* src = partial + (size_t)(off + k) * kG;
+        const float* src = partial + (size_t)slot_pos[off + k] * kG;
 #pragma unroll
         for (int i = 0; i < kG; ++i) g[i] += src[i];
     }
+#pragma unroll
+    for (int i = 0; i < kG; ++i) g_rank[(size_t)r * kG + i] = g[i];
+}
+
+// Per splat, in storage order (coalesced gradient stores): chain the render-space
+// gradients of its rank into the stored parametrisation (raster_backward.py:126-152).
+// grads layout (float32, n = scene size):
+//   [d_means (n,2) | d_log_scales (n,2) | d_rotations (n) | d_opacity_logits (n) | d_colors (n,3)]
+__global__ void chain_kernel(int64_t n, const int32_t* __restrict__ rank_of, const float* __restrict__ g_rank,
+                             const double* __restrict__ ls, const double* __restrict__ rot,
+                             const double* __restrict__ sigma_r, double kx, double ky, int accumulate,
+                             float* __restrict__ grads) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int64_t r = rank_of[s];
+    float g[kG];
+#pragma unroll
+    for (int i = 0; i < kG; ++i) g[i] = g_rank[(size_t)r * kG + i];
     const double sg = sigma_r[r];
     const double d_sigma = (double)g[3] / sg;
     const double dn00 = (double)g[6] / (2.0 * kx * kx);
@@ -392,7 +401,8 @@ int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, con
     const size_t nn = (size_t)(L.n > 0 ? L.n : 1), cc = (size_t)(L.cap > 0 ? L.cap : 1);
     float* partial = (float*)bws;
     if (L.n == 0) return SPLAT_OK;
-    SPLAT_CUDA_CHECK(cudaMemsetAsync(partial, 0, cc * kG * 4, stream));
+    float* g_rank = (float*)(bws + ((cc * kG * 4 + 255) & ~size_t(255)));
+    (void)nn;
     BwdArgs a;
     a.sc = sc;
     a.vc = vc;
@@ -417,10 +427,13 @@ int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, con
     }
     raster_bwd_kernel<<<L.ntx * L.nty, kBlock, sizeof(BwdShared), stream>>>(a); note_launch();
     const int blocks = (int)((L.n + 255) / 256);
-    reduce_chain_kernel<<<blocks, 256, 0, stream>>>(L.n, sc.rank_of, (const uint32_t*)(ws + L.touched),
-                                                    (const uint32_t*)(ws + L.offsets), partial, L.cap,
-                                                    scene.log_scales, scene.rotations, sc.sigma, vc.kx, vc.ky,
-                                                    accumulate, grads); note_launch();
+    reduce_pairs_kernel<<<blocks, 256, 0, stream>>>(L.n, (const uint32_t*)(ws + L.touched),
+                                                    (const uint32_t*)(ws + L.offsets),
+                                                    (const uint32_t*)(ws + L.slot_pos), partial, L.cap, g_rank);
+    note_launch();
+    chain_kernel<<<blocks, 256, 0, stream>>>(L.n, sc.rank_of, g_rank, scene.log_scales, scene.rotations, sc.sigma,
+                                             vc.kx, vc.ky, accumulate, grads);
+    note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
