@@ -85,7 +85,7 @@ __device__ __forceinline__ float warp_reduce9(const float (&g)[kG], int lane, fl
 // writes the (splat, tile) partials, then releases the slot for batch + kRing.
 // Warps thus drift up to kRing batches apart instead of meeting at a block
 // barrier after every batch (their per-batch work differs with coverage).
-constexpr int kRing = 4;
+constexpr int kRing = 8;
 
 struct BwdShared {
     PackF pack[kWarps_bw][kBwBatch];
@@ -190,8 +190,7 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
         uint32_t touched = 0;
         // wait until the slot's previous batch has been reduced
         if (lane == 0)
-            while (*(volatile int*)&S.epoch[slot] != round) {
-            }
+            while (*(volatile int*)&S.epoch[slot] != round) __nanosleep(64);
         __syncwarp();
         __threadfence_block();
         float(*s_part)[kG] = S.part[slot][warp];

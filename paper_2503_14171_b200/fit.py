@@ -23,14 +23,15 @@ import numpy as np
 import torch
 
 from . import _lib
-from .core import DimensionError, ParameterError
+from .core import DimensionError, ParameterError, Scene, logit
 from .device import DeviceScene, to_device
 from .distributed import allreduce_grads
 from .raster_backward import GradBuffer, PixelAdjoint, render_backward
 from .raster_forward import render_forward
 from .spline import fd_gradients, fd_gradients_backward, upscale_backward, upscale_spline
 
-UPSCALE_MODES = ("spline_analytic", "bicubic_fd")   # fit.py:23 (minus "none": no upscaling)
+UPSCALE_MODES = ("spline_analytic", "bicubic_fd")   # ViewTrainer (fit.py:23 minus "none")
+FIT_UPSCALE_MODES = ("spline_analytic", "bicubic_fd", "none")   # fit.py:23
 
 DEFAULT_LEARNING_RATES = {       # fit.py:25-31
     "means": 2e-3,               # in normalized image units; scaled by max(W, H)
@@ -203,3 +204,190 @@ class ViewTrainer:
         adam_step(scene_params(ds), grads_dict(self.grads), self.state, self.lrs)
         ds.refresh()   # view-independent terms for the updated parameters (depth order is fixed)
         return self.values
+
+
+# ---- the single-image fit driver: fit.py:37-245 --------------------------
+
+@dataclass
+class FitConfig:
+    """fit.py:37-61, same fields, defaults and validation."""
+
+    iterations: int = 1000
+    num_gaussians: int = 100
+    render_scale: float = 1.0
+    upscale_mode: str = "spline_analytic"
+    learning_rates: dict = field(default_factory=lambda: dict(DEFAULT_LEARNING_RATES))
+    ssim_weight: float = 0.2
+    seed: int = 0
+    log_every: int = 50
+    prune_interval: int = 0      # 0 disables opacity pruning
+    prune_opacity: float = 0.005
+
+    def __post_init__(self):
+        if self.iterations <= 0:
+            raise ParameterError("iterations must be positive")
+        if self.num_gaussians <= 0:
+            raise ParameterError("num_gaussians must be positive")
+        if self.render_scale < 1.0:
+            raise ParameterError("render_scale must be >= 1")
+        if self.upscale_mode not in FIT_UPSCALE_MODES:
+            raise ParameterError(f"upscale_mode must be one of {FIT_UPSCALE_MODES}")
+        if self.render_scale > 1.0 and self.upscale_mode == "none":
+            raise ParameterError("render_scale > 1 requires an upscale mode")
+        if not 0.0 <= self.ssim_weight <= 1.0:
+            raise ParameterError("ssim_weight must be in [0, 1]")
+
+
+@dataclass
+class FitRow:
+    """fit.py:64-74."""
+
+    iteration: int
+    loss: float
+    psnr: float
+    ssim: float
+    t_forward_ms: float
+    t_upscale_ms: float
+    t_backward_ms: float
+    t_opt_ms: float
+    t_total_ms: float = 0.0
+
+
+CSV_COLUMNS = ("iter", "loss", "psnr", "ssim", "t_forward_ms", "t_upscale_ms",
+               "t_backward_ms", "t_opt_ms")
+PSNR_CAP_DB = 99.0   # baselines.py psnr cap
+
+
+@dataclass
+class FitReport:
+    """fit.py:81-91: logged rows + the fitted scene (host, float64)."""
+
+    rows: list
+    scene: Scene
+
+    def write_csv(self, stream):
+        stream.write(",".join(CSV_COLUMNS) + "\n")
+        for r in self.rows:
+            stream.write(f"{r.iteration},{r.loss!r},{r.psnr!r},{r.ssim!r},"
+                         f"{r.t_forward_ms!r},{r.t_upscale_ms!r},"
+                         f"{r.t_backward_ms!r},{r.t_opt_ms!r}\n")
+
+
+def init_scene(target, n: int, seed: int) -> Scene:
+    """Random splats covering the image, coloured by the target underneath (fit.py:111-129).
+    Host numpy with the reference's RNG calls, so the initial scene is bit-identical."""
+    if n <= 0:
+        raise ParameterError("need at least one splat")
+    target = np.asarray(target.cpu().numpy() if torch.is_tensor(target) else target, dtype=np.float64)
+    h, w = target.shape[:2]
+    rng = np.random.default_rng(seed)
+    means = np.stack([rng.uniform(0, w, n), rng.uniform(0, h, n)], axis=1)
+    s = np.sqrt(w * h / (np.pi * n))
+    log_scales = np.full((n, 2), np.log(s))
+    px = np.clip(means[:, 0].astype(np.int64), 0, w - 1)
+    py = np.clip(means[:, 1].astype(np.int64), 0, h - 1)
+    colors = target[py, px].copy()
+    depths = rng.uniform(0.0, 1.0, n)
+    return Scene(means=means, log_scales=log_scales, rotations=np.zeros(n),
+                 opacity_logits=np.full(n, logit(0.5)), colors=colors, depths=depths,
+                 background=np.zeros(3), reference_resolution=(w, h))
+
+
+def _psnr(pred: torch.Tensor, target: torch.Tensor) -> float:
+    mse = float(((pred.double() - target.double()) ** 2).mean().item())
+    if mse == 0.0:
+        return PSNR_CAP_DB
+    return float(min(10.0 * np.log10(1.0 / mse), PSNR_CAP_DB))
+
+
+def _prune(ds: DeviceScene, state: AdamState, keep: torch.Tensor):
+    """Drop splats (fit.py:227-236): same depth keys, so the surviving order is unchanged."""
+    fields = {f: getattr(ds, f)[keep].contiguous()
+              for f in ("means", "log_scales", "rotations", "opacity_logits", "colors", "depths")}
+    nd = DeviceScene(**fields, background=ds.background, reference_resolution=ds.reference_resolution).prepare()
+    ns = AdamState(m={k: v[keep].contiguous() for k, v in state.m.items()},
+                   v={k: v[keep].contiguous() for k, v in state.v.items()}, t=state.t)
+    return nd, ns
+
+
+def fit(target, cfg: FitConfig, *, threads: int = 1) -> FitReport:
+    """Optimise a fresh scene against ``target`` (fit.py:163-245), every step on the GPU:
+    render (training state) -> spline / FD upscale or clip -> L1+SSIM and adjoint ->
+    upscale backward -> rasterizer backward -> Adam (float64 params) -> optional pruning.
+    Rows are logged every ``log_every`` iterations (the only host synchronisations)."""
+    del threads
+    tgt_host = np.asarray(target.cpu().numpy() if torch.is_tensor(target) else target, dtype=np.float64)
+    if tgt_host.size == 0:
+        raise DimensionError("target image is empty")
+    h, w = tgt_host.shape[:2]
+    ssim_ok = h >= SSIM_WINDOW and w >= SSIM_WINDOW
+    if cfg.ssim_weight > 0.0 and not ssim_ok:
+        raise DimensionError("target too small for the SSIM window; set ssim_weight=0")
+    low_w = max(1, int(np.floor(w / cfg.render_scale + 0.5)))
+    low_h = max(1, int(np.floor(h / cfg.render_scale + 0.5)))
+    upscaling = cfg.upscale_mode != "none" and (low_w, low_h) != (w, h)
+
+    scene = init_scene(tgt_host, cfg.num_gaussians, cfg.seed)
+    ds = DeviceScene.from_host(scene)
+    tgt = _tensor(tgt_host, ds.device)
+    lrs = dict(cfg.learning_rates)
+    lrs["means"] = lrs["means"] * max(w, h)
+    state = AdamState.like(scene_params(ds))
+    value = torch.zeros(2, dtype=torch.float64, device=ds.device)
+    metric = torch.zeros(2, dtype=torch.float64, device=ds.device)
+    adj_img = torch.empty((h, w, 3), dtype=torch.float32, device=ds.device)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    rows = []
+    for it in range(cfg.iterations):
+        ev[0].record()
+        fwd = render_forward(ds, low_w, low_h, train=True)
+        ev[1].record()
+        if upscaling:
+            src = fwd if cfg.upscale_mode == "spline_analytic" else fd_gradients(fwd.color)
+            pred = upscale_spline(src, cfg.render_scale, out_size=(w, h))
+        else:
+            src = fwd
+            pred = upscale_spline(fwd, 1.0)   # factor 1 = clip(colour), fit.py:200
+        ev[2].record()
+        loss_device(pred, tgt, cfg.ssim_weight, adj=adj_img, value=value)
+        if upscaling:
+            sadj = upscale_backward(src, cfg.render_scale, adj_img, out_size=(w, h))
+            if cfg.upscale_mode == "bicubic_fd":
+                adj = PixelAdjoint.zeros(low_w, low_h, ds.device)
+                adj.planes[:, :, 0, :] = fd_gradients_backward(sadj)
+            else:
+                adj = PixelAdjoint.from_source(sadj)
+        else:
+            adj = PixelAdjoint.zeros(low_w, low_h, ds.device)
+            adj.planes[:, :, 0, :] = adj_img
+        gb = GradBuffer(ds.n, ds.device)
+        render_backward(ds, fwd, adj, out=gb, check_finite=False)
+        ev[3].record()
+        adam_step(scene_params(ds), grads_dict(gb), state, lrs)
+        ds.refresh()
+        if (cfg.prune_interval > 0 and (it + 1) % cfg.prune_interval == 0 and it + 1 < cfg.iterations):
+            keep = 1.0 / (1.0 + torch.exp(-ds.opacity_logits)) >= cfg.prune_opacity
+            nkeep = int(keep.sum().item())
+            if 0 < nkeep < ds.n:
+                ds, state = _prune(ds, state, keep)
+        ev[4].record()
+        if it % cfg.log_every == 0 or it == cfg.iterations - 1:
+            torch.cuda.synchronize()
+            if ssim_ok:
+                if cfg.ssim_weight > 0.0:
+                    s = float(value[1].item())
+                else:
+                    loss_device(pred, tgt, 1.0, adj=torch.empty_like(pred), value=metric)
+                    s = float(metric[1].item())
+            else:
+                s = float("nan")
+            t = [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
+            rows.append(FitRow(iteration=it, loss=float(value[0].item()), psnr=_psnr(pred, tgt), ssim=s,
+                               t_forward_ms=t[0], t_upscale_ms=t[1], t_backward_ms=t[2], t_opt_ms=t[3],
+                               t_total_ms=ev[0].elapsed_time(ev[4])))
+    if not np.isfinite(rows[-1].loss):
+        raise ParameterError("fit diverged to a non-finite loss")
+    host = {f: getattr(ds, f).cpu().numpy() for f in ("means", "log_scales", "rotations", "opacity_logits",
+                                                      "colors", "depths")}
+    return FitReport(rows=rows, scene=Scene(**host, background=np.asarray(ds.background),
+                                            reference_resolution=tuple(ds.reference_resolution)))

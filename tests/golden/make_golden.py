@@ -271,6 +271,29 @@ def io_case():
          up=up, enc_in=enc_in, enc_out=enc_out, out_w=w, out_h=h, **_scene_arrays(sc))
 
 
+def fit_cases():
+    """The single-image fit driver (reference fit.py:163-245): short runs in each
+    upscale mode with per-iteration rows and pruning, from a rendered target."""
+    tsc = _as_ref(sharp_scene(seed=2, n=120, size=48))
+    target = np.clip(rf.render_forward(tsc, 48, 32, threads=8).color, 0.0, 1.0)
+    cases = {
+        "spline": dict(iterations=6, num_gaussians=50, render_scale=2.0, upscale_mode="spline_analytic",
+                       log_every=1, prune_interval=3, prune_opacity=0.475, seed=1),
+        "fd": dict(iterations=4, num_gaussians=50, render_scale=2.0, upscale_mode="bicubic_fd",
+                   log_every=1, seed=2),
+        "none": dict(iterations=4, num_gaussians=50, render_scale=1.0, upscale_mode="none",
+                     log_every=2, ssim_weight=0.0, seed=3),
+    }
+    for name, kw in cases.items():
+        cfg = rfit.FitConfig(**kw)
+        rep = rfit.fit(target, cfg, threads=8)
+        rows = np.array([[r.iteration, r.loss, r.psnr, r.ssim] for r in rep.rows], dtype=np.float64)
+        sc = rep.scene
+        save("fit_" + name, target=target, rows=rows, cfg=np.array(repr(kw)),
+             means=sc.means, log_scales=sc.log_scales, rotations=sc.rotations,
+             opacity_logits=sc.opacity_logits, colors=sc.colors, depths=sc.depths)
+
+
 if __name__ == "__main__":
     forward_cases()
     upscale_cases()
@@ -279,3 +302,4 @@ if __name__ == "__main__":
     fd_cases()
     train_case()
     io_case()
+    fit_cases()
