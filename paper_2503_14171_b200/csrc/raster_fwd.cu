@@ -209,6 +209,9 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 // group.  Step k of the blend loop then advances every group by one of ITS
 // candidates (four candidates per warp instruction stream), which roughly
 // halves the lanes idling on candidates that miss their pixels.
+#ifndef RASTER_GROUP_EXACT
+#define RASTER_GROUP_EXACT 0
+#endif
 #ifndef RASTER_MIN_BLOCKS
 #define RASTER_MIN_BLOCKS 5
 #endif
@@ -290,6 +293,13 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                 if (base + lane < end) {
                     const PackF g = s_pack[warp][b][lane];
                     if (ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
+#if RASTER_GROUP_EXACT
+                        // groups: the exact ellipse test against each 4x2 rectangle
+                        gmask = (ellipse_hits_rect(g, X0, X0 + 3.f, Y0, Y0 + 1.f) ? 1u : 0u) |
+                                (ellipse_hits_rect(g, X0 + 4.f, X0 + 7.f, Y0, Y0 + 1.f) ? 2u : 0u) |
+                                (ellipse_hits_rect(g, X0, X0 + 3.f, Y0 + 2.f, Y0 + 3.f) ? 4u : 0u) |
+                                (ellipse_hits_rect(g, X0 + 4.f, X0 + 7.f, Y0 + 2.f, Y0 + 3.f) ? 8u : 0u);
+#else
                         // groups: the cull ellipse's extent box against each 4x2 rectangle
                         const float lx = g.mxh - g.ex, hx = g.mxh + g.ex;
                         const float ly = g.myh - g.ey, hy = g.myh + g.ey;
@@ -298,6 +308,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                         const uint32_t r0 = (ly <= Y0 + 1.f && hy >= Y0) ? 1u : 0u;
                         const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
                         gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
+#endif
                     }
                 }
                 int cnt_my = 0, cnt_max = 0;
@@ -335,23 +346,36 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
     }
 }
 
-// Exact re-render of flagged pixels: one CTA per pixel.  The CTA's 256
-// threads evaluate up to kFixSeg candidates of the tile list in parallel
-// (certified float32 screen, exact float64 reference test for the survivors)
-// into shared memory; warp 0 then walks them in list order, running the
-// reference's float64 accumulation `acc = acc + alpha * (1 - acc)` for the
-// termination decision (_kernels.py:105-111) and the same float32 (or TRAIN
-// float64) value recurrences as the main pass.
-constexpr int kFixSeg = 1024;
+// Exact re-render of flagged pixels: one CTA per pixel.  Per segment of up to
+// kFixSeg candidates of the tile list:
+//   A. all threads screen their candidates with the certified float32 test
+//      (loads of 4 candidates per thread issued back to back);
+//   B. the survivors, compacted in list order, get the exact float64
+//      reference test (_kernels.py:61-80) spread over the whole CTA;
+//   C. warp 0 walks the contributors in list order, running the reference's
+//      float64 accumulation `acc = acc + alpha * (1 - acc)` for the
+//      termination decision (_kernels.py:105-111) and the same float32 (or
+//      TRAIN float64) value recurrences as the main pass.
+constexpr int kFixSeg = 2048;
+constexpr int kFixThreads = 512;
+constexpr int kFixPer = kFixSeg / kFixThreads;
+
+struct FixShared {
+    double a64[kFixSeg];
+    float4 val[kFixSeg];   // al, ax, ay, axy (compacted survivors)
+    float4 col[kFixSeg];
+    uint32_t idx[kFixSeg]; // list index of each survivor
+    int8_t st[kFixSeg];
+    uint32_t wcount[kFixThreads / 32];
+    int nsurv;
+    int done;
+};
 
 template <bool TRAIN>
-__global__ void __launch_bounds__(256) fixup_kernel(RasterArgs p) {
-    __shared__ double s_a64[kFixSeg];
-    __shared__ float4 s_val[kFixSeg];    // al, ax, ay, axy
-    __shared__ float4 s_col[kFixSeg];
-    __shared__ int8_t s_st[kFixSeg];
-    __shared__ int s_done;
-    const int tid = threadIdx.x, lane = tid & 31;
+__global__ void __launch_bounds__(kFixThreads) fixup_kernel(RasterArgs p) {
+    extern __shared__ __align__(16) unsigned char fix_raw[];
+    FixShared& S = *reinterpret_cast<FixShared*>(fix_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t nfix = p.counters[2];
     for (uint32_t w = blockIdx.x; w < nfix; w += gridDim.x) {
         const uint32_t pix = p.fixup[w];
@@ -363,50 +387,88 @@ __global__ void __launch_bounds__(256) fixup_kernel(RasterArgs p) {
         s.init();
         s.last = start;
         double acc = 0.0;
-        if (tid == 0) s_done = 0;
+        if (tid == 0) S.done = 0;
         for (uint32_t seg = start; seg < end; seg += kFixSeg) {
             const int nseg = (int)min((uint32_t)kFixSeg, end - seg);
-            for (int i = tid; i < nseg; i += blockDim.x) {
-                const uint32_t r = p.ranks[seg + i];
-                const PackF g = p.pack[r];
-                float al = 0.f, gax = 0.f, gay = 0.f, gaxy = 0.f, rel;
-                double a64 = 0.0;
-                int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
-                if (st != kCulled) {
-                    st = eval_exact_inl(p.sc, p.vc, p.bboxes, r, px, py, &a64);
-                    if (st != kCulled) {
-                        canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
-                        s_col[i] = p.sc.color[r];
-                    }
+            // A: float32 screen; candidate i = tid * kFixPer + u keeps list order per thread
+            uint32_t rr[kFixPer];
+#pragma unroll
+            for (int u = 0; u < kFixPer; ++u) {
+                const int i = tid * kFixPer + u;
+                rr[u] = i < nseg ? p.ranks[seg + i] : 0u;
+            }
+            uint32_t keepm = 0;
+#pragma unroll
+            for (int u = 0; u < kFixPer; ++u) {
+                const int i = tid * kFixPer + u;
+                if (i < nseg) {
+                    const PackF g = p.pack[rr[u]];
+                    float al, gax, gay, gaxy, rel;
+                    if (eval_fast(g, cx, cy, al, gax, gay, gaxy, rel) != kCulled) keepm |= 1u << u;
                 }
-                s_st[i] = (int8_t)st;
-                s_a64[i] = a64;
-                s_val[i] = make_float4(al, gax, gay, gaxy);
+            }
+            // compact the survivors in list order (block-wide exclusive scan of popcounts)
+            const uint32_t cnt = __popc(keepm);
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            if (lane == 31) S.wcount[wid] = incl;
+            __syncthreads();
+            uint32_t base = 0, total = 0;
+#pragma unroll
+            for (int k = 0; k < kFixThreads / 32; ++k) {
+                const uint32_t c = S.wcount[k];
+                base += k < wid ? c : 0u;
+                total += c;
+            }
+            base += incl - cnt;
+#pragma unroll
+            for (int u = 0; u < kFixPer; ++u)
+                if ((keepm >> u) & 1u) S.idx[base++] = (uint32_t)(tid * kFixPer + u);
+            __syncthreads();
+            // B: exact float64 test of the survivors, spread over the CTA
+            for (uint32_t k = tid; k < total; k += kFixThreads) {
+                const uint32_t i = S.idx[k];
+                const uint32_t r = p.ranks[seg + i];
+                double a64 = 0.0;
+                float al = 0.f, gax = 0.f, gay = 0.f, gaxy = 0.f;
+                int st = eval_exact_inl(p.sc, p.vc, p.bboxes, r, px, py, &a64);
+                if (st != kCulled) {
+                    canonical_values(p.pack[r], cx, cy, st, al, gax, gay, gaxy);
+                    S.col[k] = p.sc.color[r];
+                }
+                S.st[k] = (int8_t)st;
+                S.a64[k] = a64;
+                S.val[k] = make_float4(al, gax, gay, gaxy);
             }
             __syncthreads();
+            // C: the reference's ordered accumulation
             if (tid < 32) {
                 bool done = false;
-                for (int c0 = 0; c0 < nseg && !done; c0 += 32) {
-                    uint32_t bits = __ballot_sync(0xffffffffu, c0 + lane < nseg && s_st[c0 + lane] != kCulled);
+                for (uint32_t c0 = 0; c0 < total && !done; c0 += 32) {
+                    uint32_t bits = __ballot_sync(0xffffffffu, c0 + lane < total && S.st[c0 + lane] != kCulled);
                     while (bits) {
-                        const int k = c0 + __ffs(bits) - 1;
+                        const uint32_t k = c0 + __ffs(bits) - 1;
                         bits &= bits - 1;
-                        const float4 v = s_val[k];
-                        const float om = s_st[k] == kClamped ? 1.0e-3f : 1.f - v.x;
-                        s.add(v.x, v.y, v.z, v.w, om, s_col[k]);
-                        s.last = seg + k + 1;
+                        const float4 v = S.val[k];
+                        const float om = S.st[k] == kClamped ? 1.0e-3f : 1.f - v.x;
+                        s.add(v.x, v.y, v.z, v.w, om, S.col[k]);
+                        s.last = seg + S.idx[k] + 1;
                         const double t = __dsub_rn(1.0, acc);
-                        acc = __dadd_rn(acc, __dmul_rn(s_a64[k], t));
+                        acc = __dadd_rn(acc, __dmul_rn(S.a64[k], t));
                         if (__dsub_rn(1.0, acc) < kEarlyTerm) {
                             done = true;
                             break;
                         }
                     }
                 }
-                if (lane == 0 && done) s_done = 1;
+                if (lane == 0 && done) S.done = 1;
             }
             __syncthreads();
-            if (s_done) break;
+            if (S.done) break;
         }
         if (tid == 0) write_pixel<TRAIN>(p, px, py, s);
         __syncthreads();
@@ -443,16 +505,20 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
         grid_inf = max(per_sm, 1) * sms;
         SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<true>, kRasterThreads, 0));
         grid_train = max(per_sm, 1) * sms;
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fixup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sizeof(FixShared)));
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fixup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sizeof(FixShared)));
     }
     const int ntiles = L.ntx * L.nty;
     // counters[2] = fix-up pixels, counters[3] = work-unit cursor of the persistent raster
     SPLAT_CUDA_CHECK(cudaMemsetAsync(a.counters + 2, 0, 8, stream));
     if (train) {
         raster_fwd_kernel<true><<<grid_train, kRasterThreads, 0, stream>>>(a); note_launch();
-        fixup_kernel<true><<<148 * 4, 256, 0, stream>>>(a); note_launch();
+        fixup_kernel<true><<<148 * 2, kFixThreads, sizeof(FixShared), stream>>>(a); note_launch();
     } else {
         raster_fwd_kernel<false><<<grid_inf, kRasterThreads, 0, stream>>>(a); note_launch();
-        fixup_kernel<false><<<148 * 4, 256, 0, stream>>>(a); note_launch();
+        fixup_kernel<false><<<148 * 2, kFixThreads, sizeof(FixShared), stream>>>(a); note_launch();
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
