@@ -676,6 +676,97 @@ __global__ void __launch_bounds__(256) upscale_bwd_kernel(const float* __restric
     }
 }
 
+// Exact-x4 backward (out = 4 x in on both axes): source pixel x is corner b of
+// cell x-1 for outputs 4x-2..4x+1 (phases 0..3) and corner a of cell x for
+// outputs 4x+2..4x+5; at the borders the clamped corner coincides with x and
+// both weights apply (the transpose of the edge replication, spline.py:232-243).
+// Per CTA: 32 x 8 source pixels.  x pass: each warp stages whole output-row
+// segments of the adjoint (coalesced) in shared memory and every lane contracts
+// its source column's 8-wide window into value / slope partial sums; y pass: one
+// source pixel per thread contracts 8 rows of those.
+constexpr int kB4Cols = 32, kB4Rows = 8;
+constexpr int kB4WinC = 4 * kB4Cols + 8, kB4WinR = 4 * kB4Rows + 8;
+
+__device__ __forceinline__ void x4_weights(int j, int x, int n, float& wv, float& ws) {
+    if (j < 4) {   // x = corner b of cell x-1, phase j
+        wv = hermite_w(4, j, 1);
+        ws = hermite_w(4, j, 3);
+        if (x == 0) {   // cell -1: corner a clamps onto x as well
+            wv += hermite_w(4, j, 0);
+            ws += hermite_w(4, j, 2);
+        }
+    } else {       // x = corner a of cell x, phase j-4
+        wv = hermite_w(4, j - 4, 0);
+        ws = hermite_w(4, j - 4, 2);
+        if (x == n - 1) {   // cell n-1: corner b clamps onto x as well
+            wv += hermite_w(4, j - 4, 1);
+            ws += hermite_w(4, j - 4, 3);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) upscale_bwd_x4_kernel(const float* __restrict__ adj,
+                                                             float* __restrict__ dsrc, int in_w, int in_h) {
+    __shared__ float s_row[8][kB4WinC * 3];
+    __shared__ float s_g[kB4WinR][kB4Cols][6];
+    const int out_w = 4 * in_w, out_h = 4 * in_h;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int X0 = blockIdx.x * kB4Cols, Y0 = blockIdx.y * kB4Rows;
+    const int u0 = 4 * X0 - 2, v0 = 4 * Y0 - 2;
+    const int x = X0 + lane;
+    float wv[8], ws[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x4_weights(j, x, in_w, wv[j], ws[j]);
+    for (int vi = warp; vi < kB4WinR; vi += 8) {
+        const int v = v0 + vi;
+        float* row = s_row[warp];
+        const bool vok = v >= 0 && v < out_h;
+        for (int e = lane; e < kB4WinC * 3; e += 32) {
+            const int u = u0 + e / 3;
+            row[e] = (vok && u >= 0 && u < out_w) ? __ldg(adj + ((size_t)v * out_w + u0) * 3 + e) : 0.f;
+        }
+        __syncwarp();
+        float a[3] = {0.f, 0.f, 0.f}, b[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float* g = row + (4 * lane + j) * 3;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                a[c] = fmaf(wv[j], g[c], a[c]);
+                b[c] = fmaf(ws[j], g[c], b[c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            s_g[vi][lane][c] = a[c];
+            s_g[vi][lane][3 + c] = b[c];
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    const int yi = threadIdx.x >> 5, xi = lane;
+    const int y = Y0 + yi;
+    if (y >= in_h || x >= in_w) return;
+    float f[3] = {0, 0, 0}, fx[3] = {0, 0, 0}, fy[3] = {0, 0, 0}, fxy[3] = {0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float hv, hs;
+        x4_weights(i, y, in_h, hv, hs);
+        const float* d = s_g[4 * yi + i][xi];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            f[c] = fmaf(hv, d[c], f[c]);
+            fy[c] = fmaf(hs, d[c], fy[c]);
+            fx[c] = fmaf(hv, d[3 + c], fx[c]);
+            fxy[c] = fmaf(hs, d[3 + c], fxy[c]);
+        }
+    }
+    float4* o = reinterpret_cast<float4*>(dsrc + ((size_t)y * in_w + x) * 12);
+    o[0] = make_float4(f[0], f[1], f[2], fx[0]);
+    o[1] = make_float4(fx[1], fx[2], fy[0], fy[1]);
+    o[2] = make_float4(fy[2], fxy[0], fxy[1], fxy[2]);
+}
+
 // ---- finite-difference derivative planes (spline.py:246-297) -----------------
 
 __device__ __forceinline__ float diff1(const float* f, int i, int n, int stride) {
@@ -871,16 +962,23 @@ int upscale_backward_impl(const float* adj, int out_w, int out_h, float* dsrc, i
     int max_u = (int)ceil((kBwCols + 2) * sx) + 8;
     int max_v = (int)ceil((kBwRows + 2) * sy) + 8;
     size_t smem = (size_t)(max_u + max_v) * sizeof(AxisMap) + (size_t)max_v * kBwCols * 6 * 4;
+    if (out_w == 4 * in_w && out_h == 4 * in_h) {   // the x4 training path (C5)
+        dim3 g4(ceil_div(in_w, kB4Cols), ceil_div(in_h, kB4Rows));
+        upscale_bwd_x4_kernel<<<g4, 256, 0, stream>>>(adj, dsrc, in_w, in_h);
+        note_launch();
+        SPLAT_CUDA_CHECK(cudaGetLastError());
+        return SPLAT_OK;
+    }
     static int configured = 0;
     if (!configured) {
-        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_bwd_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              200 * 1024));
         configured = 1;
     }
     if (smem > 200 * 1024) return set_error(SPLAT_ERR_DIMENSION, "upscale backward tile too large");
     dim3 grid(ceil_div(in_w, kBwCols), ceil_div(in_h, kBwRows));
-    upscale_bwd_kernel<<<grid, 256, smem, stream>>>(adj, out_w, out_h, dsrc, in_w, in_h, sx, sy, max_u,
-                                                    max_v); note_launch();
+    upscale_bwd_kernel<<<grid, 256, smem, stream>>>(adj, out_w, out_h, dsrc, in_w, in_h, sx, sy, max_u, max_v);
+    note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
