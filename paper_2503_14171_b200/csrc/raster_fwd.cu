@@ -209,6 +209,12 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 // group.  Step k of the blend loop then advances every group by one of ITS
 // candidates (four candidates per warp instruction stream), which roughly
 // halves the lanes idling on candidates that miss their pixels.
+#ifndef RASTER_TERM_MASK
+#define RASTER_TERM_MASK 7
+#endif
+#ifndef RASTER_STATS
+#define RASTER_STATS 0
+#endif
 #ifndef RASTER_GROUP_EXACT
 #define RASTER_GROUP_EXACT 0
 #endif
@@ -312,6 +318,9 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                     }
                 }
                 int cnt_my = 0, cnt_max = 0;
+#if RASTER_STATS
+                int cnt_sum = 0;
+#endif
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
                     const uint32_t mq = __ballot_sync(0xffffffffu, (gmask >> qq) & 1u);
@@ -319,16 +328,32 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                     const int c = __popc(mq);
                     cnt_max = max(cnt_max, c);
                     if (qq == q) cnt_my = c;
+#if RASTER_STATS
+                    cnt_sum += c;
+#endif
                 }
+#if RASTER_STATS
+                if (lane == 0) {
+                    atomicAdd((unsigned long long*)&p.counters[8], 1ull);
+                    atomicAdd((unsigned long long*)&p.counters[10], (unsigned long long)cnt_max);
+                    atomicAdd((unsigned long long*)&p.counters[12], (unsigned long long)cnt_sum);
+                }
+#endif
                 __syncwarp();
                 for (int k = 0; k < cnt_max; ++k) {
+#if RASTER_STATS
+                    {
+                        const uint32_t ev = __ballot_sync(0xffffffffu, active && k < cnt_my);
+                        if (lane == 0) atomicAdd((unsigned long long*)&p.counters[14], (unsigned long long)__popc(ev));
+                    }
+#endif
                     if (active && k < cnt_my) {
                         const int idx = s_list[warp][q][k];
                         blend_candidate<TRAIN>(p, s_pack[warp][b][idx], s_col[warp][b][idx],
                                                s_rank[warp][b][idx], base + idx, px, py, cx, cy, s, active,
                                                flagged);
                     }
-                    if ((k & 7) == 7 && !__any_sync(0xffffffffu, active)) break;
+                    if ((k & RASTER_TERM_MASK) == RASTER_TERM_MASK && !__any_sync(0xffffffffu, active)) break;
                 }
                 if (!__any_sync(0xffffffffu, active)) break;
                 __syncwarp();
