@@ -169,6 +169,11 @@ int splat_loss(const float *pred, const float *target, int width, int height, do
 int splat_adam_step(double *params, const float *grads, double *m, double *v, int64_t count, double lr,
                     double beta1, double beta2, double bc1, double bc2, double eps, void *stream);
 
+/* dst += src over `count` floats: folds per-stream gradient buffers (views
+ * rendered concurrently) into one in a fixed order (deterministic sum of the
+ * per-view gradients, raster_backward.py's outputs summed over views). */
+int splat_grad_accumulate(float *dst, const float *src, int64_t count, void *stream);
+
 /* ---- spline upscaler ----------------------------------------------------
  * upscale_spline (spline.py:162-178): (H,W,4,3) gradient planes -> (Ho,Wo,3).
  * upscale_backward (spline.py:191-243): (Ho,Wo,3) adjoint -> (H,W,4,3). */

@@ -66,6 +66,7 @@ SIGNATURES = {
     "splat_gimg_pack": (I32, [P, P, I32, I32, P, P]),
     "splat_gimg_unpack": (I32, [P, I32, I32, P, P, P, P]),
     "splat_encode_display": (I32, [P, I64, P, P]),
+    "splat_grad_accumulate": (I32, [P, P, I64, P]),
     "splat_rasterize": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
                               ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_view_pack64": (I32, [P, I64, ctypes.POINTER(ViewT), P, P]),

@@ -48,6 +48,7 @@ int gimg_pack_impl(const float* planes, const float* alpha, int w, int h, float*
 int gimg_unpack_impl(const float* in, int w, int h, float* planes, float* alpha, int32_t* count,
                      cudaStream_t stream);
 int encode_display_impl(const float* img, int64_t n, uint8_t* out, cudaStream_t stream);
+int accumulate_impl(float* dst, const float* src, int64_t n, cudaStream_t stream);
 
 static int check_dims(int width, int height) {
     if (width <= 0 || height <= 0)
@@ -254,6 +255,11 @@ int splat_gimg_unpack(const float* in, int width, int height, float* planes, flo
                       void* stream) {
     if (width <= 0 || height <= 0) return set_error(SPLAT_ERR_DIMENSION, "image dimensions must be positive");
     return gimg_unpack_impl(in, width, height, planes, alpha, count, (cudaStream_t)stream);
+}
+
+int splat_grad_accumulate(float* dst, const float* src, int64_t count, void* stream) {
+    if (count < 0) return set_error(SPLAT_ERR_DIMENSION, "negative element count");
+    return accumulate_impl(dst, src, count, (cudaStream_t)stream);
 }
 
 int splat_encode_display(const float* image, int64_t count, uint8_t* out, void* stream) {

@@ -283,7 +283,31 @@ __global__ void adam_kernel(double* __restrict__ p, const float* __restrict__ g,
     p[i] = p[i] - lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
 }
 
+// dst += src (float32): folds per-stream gradient buffers into one, in a fixed order.
+__global__ void accumulate_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t n) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i + 3 < n) {
+        float4 a = *reinterpret_cast<const float4*>(dst + i);
+        const float4 b = *reinterpret_cast<const float4*>(src + i);
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+        *reinterpret_cast<float4*>(dst + i) = a;
+    } else {
+        for (int64_t k = i; k < n; ++k) dst[k] += src[k];
+    }
+}
+
 }  // namespace
+
+int accumulate_impl(float* dst, const float* src, int64_t n, cudaStream_t stream) {
+    if (n <= 0) return SPLAT_OK;
+    const int64_t threads = (n + 3) / 4;
+    accumulate_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(dst, src, n); note_launch();
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
 
 size_t loss_workspace_bytes_impl(int w, int h) {
     size_t nparts = (size_t)ceil_div(w, kS) * ceil_div(h, kS) * 3;

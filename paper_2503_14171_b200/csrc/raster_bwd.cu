@@ -79,19 +79,60 @@ __device__ __forceinline__ float warp_reduce9(const float (&g)[kG], int lane, fl
     return v;
 }
 
+// Reduce-scatter of the nine terms over the 8 lanes of a 4x2 group (lane bits
+// 2, 1, 0): lane li of the group ends with the group sum of term li; g8 gets the
+// sum of term 8.  Fixed order, deterministic.
+__device__ __forceinline__ float group_reduce9(const float (&g)[kG], int li, float& g8) {
+    const bool b2 = li & 4, b1 = li & 2, b0 = li & 1;
+    float h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float send = b2 ? g[i] : g[i + 4];
+        const float keep = b2 ? g[i + 4] : g[i];
+        h[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    float q[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float send = b1 ? h[i] : h[i + 2];
+        const float keep = b1 ? h[i + 2] : h[i];
+        q[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    const float send = b0 ? q[0] : q[1];
+    const float keep = b0 ? q[1] : q[0];
+    const float v = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    float e = g[8];
+    e += __shfl_xor_sync(0xffffffffu, e, 4);
+    e += __shfl_xor_sync(0xffffffffu, e, 2);
+    e += __shfl_xor_sync(0xffffffffu, e, 1);
+    g8 = e;
+    return v;
+}
+
+#ifndef BWD_GROUPS
+#define BWD_GROUPS 1
+#endif
+#ifndef RING_G
+#define RING_G 4
+#endif
+
 // Batches of kBwBatch candidates are walked back to front by every warp of the
 // tile independently.  Per-batch, per-warp partials go to one of kRing shared
 // slots; the last warp to finish a batch sums its slot in fixed warp order and
 // writes the (splat, tile) partials, then releases the slot for batch + kRing.
 // Warps thus drift up to kRing batches apart instead of meeting at a block
 // barrier after every batch (their per-batch work differs with coverage).
-constexpr int kRing = 8;
+constexpr int kRing = BWD_GROUPS ? RING_G : 8;
 
 struct BwdShared {
     PackF pack[kWarps_bw][kBwBatch];
     float4 col[kWarps_bw][kBwBatch];
     uint32_t rank[kWarps_bw][kBwBatch];
     float part[kRing][kWarps_bw][kBwBatch][kG];
+#if BWD_GROUPS
+    float gpart[kWarps_bw][4][kBwBatch][kG];   // per 4x2 group partials of the current batch
+    uint8_t list[kWarps_bw][4][kBwBatch];      // per group candidate lists (ascending)
+#endif
     uint32_t touch[kRing][kWarps_bw];
     int done[kRing];
     int epoch[kRing];
@@ -109,7 +150,13 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
     const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int rx0 = tile_x * kTile + (warp & 1) * 8, ry0 = tile_y * kTile + (warp >> 1) * 4;
+#if BWD_GROUPS
+    // four 4x2 lane groups (as in the forward): group q walks its own candidate list
+    const int q = lane >> 3, li = lane & 7;
+    const int px = rx0 + (q & 1) * 4 + (li & 3), py = ry0 + (q >> 1) * 2 + (li >> 2);
+#else
     const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3);
+#endif
     const bool inside = px < p.width && py < p.height;
     const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
     const float X0 = (float)rx0 + 0.5f, Y0 = (float)ry0 + 0.5f;
@@ -186,6 +233,152 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                 s_col[warp][lane] = p.sc.color[r];
             }
         }
+#if BWD_GROUPS
+        uint32_t gmask = 0;   // bit g: candidate reaches group g's 4x2 rectangle
+        if (keep) {
+            const PackF& g = s_pack[warp][lane];
+            const float lx = g.mxh - g.ex, hx = g.mxh + g.ex;
+            const float ly = g.myh - g.ey, hy = g.myh + g.ey;
+            const uint32_t c0 = (lx <= X0 + 3.f && hx >= X0) ? 1u : 0u;
+            const uint32_t c1 = (lx <= X0 + 7.f && hx >= X0 + 4.f) ? 1u : 0u;
+            const uint32_t r0 = (ly <= Y0 + 1.f && hy >= Y0) ? 1u : 0u;
+            const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
+            gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
+        }
+        const uint32_t lt = (1u << lane) - 1u;
+        int cnt_my = 0, cnt_max = 0;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            const uint32_t mq = __ballot_sync(0xffffffffu, (gmask >> qq) & 1u);
+            if ((gmask >> qq) & 1u) S.list[warp][qq][__popc(mq & lt)] = (uint8_t)lane;
+            const int c = __popc(mq);
+            cnt_max = max(cnt_max, c);
+            if (qq == q) cnt_my = c;
+        }
+        __syncwarp();
+        uint32_t tmask = 0;   // this lane's group: candidates it produced partials for
+        for (int k = 0; k < cnt_max; ++k) {   // back to front within each group's list
+            const bool has = k < cnt_my;
+            const int idx = has ? S.list[warp][q][cnt_my - 1 - k] : 0;
+            float gr[kG];
+#pragma unroll
+            for (int i = 0; i < kG; ++i) gr[i] = 0.f;
+            bool contrib = false;
+            if (has && live && lo + idx < my_last) {
+                const PackF g = s_pack[warp][idx];
+                float al, gax, gay, gaxy, rel;
+                int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
+                if (st == kUnsure) {
+                    double a64;
+                    st = eval_exact(p.sc, p.vc, p.bboxes, s_rank[warp][idx], px, py, &a64);
+                    if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
+                }
+                if (st != kCulled) {
+                    contrib = true;
+                    const float4 col = s_col[warp][idx];
+                    const float cc[3] = {col.x, col.y, col.z};
+                    // invert the accumulated-alpha state across this splat (float64)
+                    const double om = st == kClamped ? (double)1.0e-3f : (double)(1.f - al);
+                    // 1/om: float32 reciprocal refined by two float64 Newton steps (|rel err| ~ 1e-16)
+                    double inv = (double)fast_rcp((float)om);
+                    inv = inv * fma(-om, inv, 2.0);
+                    inv = inv * fma(-om, inv, 2.0);
+                    const double Tp = T * inv;
+                    const double axp = (ax - Tp * (double)gax) * inv;
+                    const double ayp = (ay - Tp * (double)gay) * inv;
+                    const double axyp = (axy - Tp * (double)gaxy + axp * (double)gay + ayp * (double)gax) * inv;
+                    const float t = (float)Tp, sx = (float)axp, sy = (float)ayp, sxy = (float)axyp;
+                    float abar = 0.f, abar_x = 0.f, abar_y = 0.f, abar_xy = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float W0 = w[c], WX = w[3 + c], WY = w[6 + c], WXY = w[9 + c];
+                        const float diff = cc[c] - bh[c];
+                        const float u0 = t * diff;
+                        const float u1 = -sx * diff - t * bhx[c];
+                        const float u2 = -sy * diff - t * bhy[c];
+                        const float u3 = ((-sxy * diff + sx * bhy[c]) + sy * bhx[c]) - t * bhxy[c];
+                        // _kernels.py:253-262
+                        gr[c] = W0 * (t * al) + WX * (t * gax - sx * al) + WY * (t * gay - sy * al) +
+                                WXY * (((t * gaxy - sxy * al) - sy * gax) - sx * gay);
+                        abar += W0 * u0 + WX * u1 + WY * u2 + WXY * u3;
+                        abar_x += WX * u0 + WXY * u2;
+                        abar_y += WY * u0 + WXY * u1;
+                        abar_xy += WXY * u0;
+                    }
+                    if (st != kClamped) {   // _kernels.py:291-336
+                        const float dx = (cx - g.mxh) - g.mxl, dy = (cy - g.myh) - g.myl;
+                        const float ca = g.a, cb = g.b, ccn = g.c;
+                        const float gx = -(2.f * ca * dx + 2.f * cb * dy);
+                        const float gy = -(2.f * cb * dx + 2.f * ccn * dy);
+                        const float hxy = gx * gy - 2.f * cb;
+                        gr[3] = abar * al + abar_x * gax + abar_y * gay + abar_xy * gaxy;   // / sigma later
+                        gr[4] = al * (abar * (-gx) + abar_x * (-gx * gx + 2.f * ca) + abar_y * (-gx * gy + 2.f * cb) +
+                                      abar_xy * (-gx * hxy + 2.f * ca * gy + 2.f * cb * gx));
+                        gr[5] = al * (abar * (-gy) + abar_x * (-gy * gx + 2.f * cb) + abar_y * (-gy * gy + 2.f * ccn) +
+                                      abar_xy * (-gy * hxy + 2.f * cb * gy + 2.f * ccn * gx));
+                        const float dxx = dx * dx, dxy2 = 2.f * dx * dy, dyy = dy * dy;
+                        gr[6] = al * (abar * (-dxx) + abar_x * (-dxx * gx - 2.f * dx) + abar_y * (-dxx * gy) +
+                                      abar_xy * (-dxx * hxy - 2.f * dx * gy));
+                        gr[7] = al * (abar * (-dxy2) + abar_x * (-dxy2 * gx - 2.f * dy) +
+                                      abar_y * (-dxy2 * gy - 2.f * dx) +
+                                      abar_xy * (((-dxy2 * hxy - 2.f * dy * gy) - 2.f * gx * dx) - 2.f));
+                        gr[8] = al * (abar * (-dyy) + abar_x * (-dyy * gx) + abar_y * (-dyy * gy - 2.f * dy) +
+                                      abar_xy * (-dyy * hxy - 2.f * dy * gx));
+                    }
+                    // advance the behind-colour state through this splat (_kernels.py:337-357)
+                    const float omf = (float)om;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float dcb = cc[c] - bh[c];
+                        const float nbx = omf * bhx[c] + gax * dcb;
+                        const float nby = omf * bhy[c] + gay * dcb;
+                        const float nbxy = ((omf * bhxy[c] + gaxy * dcb) - gay * bhx[c]) - gax * bhy[c];
+                        bh[c] = omf * bh[c] + al * cc[c];
+                        bhx[c] = nbx;
+                        bhy[c] = nby;
+                        bhxy[c] = nbxy;
+                    }
+                    T = Tp;
+                    ax = axp;
+                    ay = ayp;
+                    axy = axyp;
+                }
+            }
+            const uint32_t cb = __ballot_sync(0xffffffffu, contrib);
+            if (cb) {
+                float g8;
+                const float v = group_reduce9(gr, li, g8);
+                if ((cb >> (q * 8)) & 0xffu) {
+                    S.gpart[warp][q][idx][li] = v;
+                    if (li == 0) S.gpart[warp][q][idx][8] = g8;
+                    tmask |= 1u << idx;
+                }
+            }
+        }
+        __syncwarp();
+        uint32_t gm[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) gm[g] = __shfl_sync(0xffffffffu, tmask, g * 8);
+        const uint32_t touched = gm[0] | gm[1] | gm[2] | gm[3];
+        // wait until the slot's previous batch has been reduced
+        if (lane == 0)
+            while (*(volatile int*)&S.epoch[slot] != round) __nanosleep(64);
+        __syncwarp();
+        __threadfence_block();
+        if ((touched >> lane) & 1u) {   // this warp's partial of candidate `lane`, groups in fixed order
+            float acc[kG];
+#pragma unroll
+            for (int i = 0; i < kG; ++i) acc[i] = 0.f;
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+                if ((gm[g] >> lane) & 1u) {
+#pragma unroll
+                    for (int i = 0; i < kG; ++i) acc[i] += S.gpart[warp][g][lane][i];
+                }
+#pragma unroll
+            for (int i = 0; i < kG; ++i) S.part[slot][warp][lane][i] = acc[i];
+        }
+#else
         uint32_t bits = __ballot_sync(0xffffffffu, keep);
         uint32_t touched = 0;
         // wait until the slot's previous batch has been reduced
@@ -290,6 +483,7 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                 touched |= 1u << k;
             }
         }
+#endif
         // publish; the last warp of the batch reduces the slot
         int prev = 0;
         if (lane == 0) {

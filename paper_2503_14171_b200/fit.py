@@ -53,13 +53,14 @@ def _tensor(a, device=None):
 
 
 def loss_device(pred: torch.Tensor, target: torch.Tensor, ssim_weight: float,
-                adj: torch.Tensor | None = None, value: torch.Tensor | None = None):
-    """Loss on the device without a host sync: returns (value (2,) float64 [loss, ssim], adjoint)."""
+                adj: torch.Tensor | None = None, value: torch.Tensor | None = None, slot: int = 0):
+    """Loss on the device without a host sync: returns (value (2,) float64 [loss, ssim], adjoint).
+    ``slot`` selects a private workspace (one per concurrently used stream)."""
     if tuple(pred.shape) != tuple(target.shape):
         raise DimensionError("prediction and target dimensions differ")
     h, w = int(pred.shape[0]), int(pred.shape[1])
     lib = _lib.load()
-    key = (w, h, str(pred.device))
+    key = (w, h, str(pred.device), slot)
     ws = _loss_ws.get(key)
     if ws is None:
         ws = torch.empty(lib.splat_loss_workspace_bytes(w, h), dtype=torch.uint8, device=pred.device)
@@ -143,6 +144,8 @@ class ViewTrainer:
     upscale_mode: str = "spline_analytic"
     lrs: dict = field(default_factory=lambda: dict(DEFAULT_LEARNING_RATES))
     group: object = None
+    streams: int = 2   # views in flight at once (the rasterizer backward of one view has
+                       # only W/16 x H/16 tile CTAs; a second view fills the idle SMs)
 
     def __post_init__(self):
         self.ds = to_device(self.scene)
@@ -156,7 +159,11 @@ class ViewTrainer:
         self.grads = GradBuffer(self.ds.n, self.ds.device)
         self.state = AdamState.like(scene_params(self.ds))
         self.values = torch.zeros((max(len(self.views), 1), 2), dtype=torch.float64, device=self.ds.device)
-        self._adj = torch.empty((h, w, 3), dtype=torch.float32, device=self.ds.device)
+        self.streams = max(1, min(int(self.streams), max(len(self.views), 1)))
+        self._streams = [torch.cuda.Stream(device=self.ds.device) for _ in range(self.streams)]
+        self._slot_grads = [self.grads] + [GradBuffer(self.ds.n, self.ds.device) for _ in range(self.streams - 1)]
+        self._adjs = [torch.empty((h, w, 3), dtype=torch.float32, device=self.ds.device)
+                      for _ in range(self.streams)]
         self._calibrate()
 
     def _calibrate(self):
@@ -182,24 +189,42 @@ class ViewTrainer:
                                    "re-sized, repeat the step")
 
     def step(self) -> torch.Tensor:
-        """One step; returns the per-view [loss, ssim] rows (device, no host sync)."""
+        """One step; returns the per-view [loss, ssim] rows (device, no host sync).
+
+        View i runs on stream i mod ``streams`` and accumulates into that stream's
+        gradient buffer (views in order); the buffers are then folded into one in
+        stream order, so the sum is deterministic for a fixed ``streams``."""
         ds, (rw, rh), (w, h) = self.ds, self.render_size, self.out_size
-        self.grads.zero_()
+        main = torch.cuda.current_stream(ds.device)
+        for st in self._streams:
+            st.wait_stream(main)
         self._frames = []
+        for k, st in enumerate(self._streams):
+            with torch.cuda.stream(st):
+                self._slot_grads[k].zero_()
         for i, (v, tgt) in enumerate(zip(self.views, self.targets)):
-            fwd = render_forward(ds, rw, rh, view=v, train=True, sync_check=False)
-            self._frames.append(fwd.frame)
-            # fit.py:192-212: the analytic channels, or classical bicubic from FD planes
-            src = fwd if self.upscale_mode == "spline_analytic" else fd_gradients(fwd.color)
-            pred = upscale_spline(src, 1.0, out_size=(w, h))
-            loss_device(pred, tgt, self.ssim_weight, adj=self._adj, value=self.values[i])
-            sadj = upscale_backward(src, 1.0, self._adj, out_size=(w, h))
-            if self.upscale_mode == "spline_analytic":
-                adj = PixelAdjoint.from_source(sadj)
-            else:
-                adj = PixelAdjoint.zeros(rw, rh, ds.device)
-                adj.planes[:, :, 0, :] = fd_gradients_backward(sadj)
-            render_backward(ds, fwd, adj, out=self.grads, accumulate=True, check_finite=False)
+            k = i % self.streams
+            with torch.cuda.stream(self._streams[k]):
+                adj_img = self._adjs[k]
+                fwd = render_forward(ds, rw, rh, view=v, train=True, sync_check=False)
+                self._frames.append(fwd.frame)
+                # fit.py:192-212: the analytic channels, or classical bicubic from FD planes
+                src = fwd if self.upscale_mode == "spline_analytic" else fd_gradients(fwd.color)
+                pred = upscale_spline(src, 1.0, out_size=(w, h))
+                loss_device(pred, tgt, self.ssim_weight, adj=adj_img, value=self.values[i], slot=k)
+                sadj = upscale_backward(src, 1.0, adj_img, out_size=(w, h))
+                if self.upscale_mode == "spline_analytic":
+                    adj = PixelAdjoint.from_source(sadj)
+                else:
+                    adj = PixelAdjoint.zeros(rw, rh, ds.device)
+                    adj.planes[:, :, 0, :] = fd_gradients_backward(sadj)
+                render_backward(ds, fwd, adj, out=self._slot_grads[k], accumulate=True, check_finite=False)
+        for st in self._streams:
+            main.wait_stream(st)
+        lib = _lib.load()
+        for k in range(1, self.streams):
+            _lib.check(lib.splat_grad_accumulate(_lib.ptr(self.grads.flat), _lib.ptr(self._slot_grads[k].flat),
+                                                 self.grads.flat.numel(), _lib.stream_ptr(main)))
         allreduce_grads(self.grads.flat, self.group)
         adam_step(scene_params(ds), grads_dict(self.grads), self.state, self.lrs)
         ds.refresh()   # view-independent terms for the updated parameters (depth order is fixed)

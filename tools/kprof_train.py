@@ -8,13 +8,14 @@ from paper_2503_14171_b200.scenes import CONFIGS, random_views, synthetic_scene
 
 vpr = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+streams = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 c = CONFIGS["c5"]
 model = synthetic_scene(c.n, c.canvas_w, c.canvas_h, c.scale_range, seed=5)
 target = synthetic_scene(c.n, c.canvas_w, c.canvas_h, c.scale_range, seed=7)
 views = random_views(vpr, c.canvas_w, c.canvas_h, seed=13)
 W, H = c.out_size
 targets = [render_forward(target, W, H, view=v).color.clamp(0.0, 1.0).contiguous() for v in views]
-tr = fit.ViewTrainer(model, (c.width, c.height), (W, H), views, targets, ssim_weight=0.2)
+tr = fit.ViewTrainer(model, (c.width, c.height), (W, H), views, targets, ssim_weight=0.2, streams=streams)
 for _ in range(2):
     tr.step()
 torch.cuda.synchronize()
@@ -35,4 +36,11 @@ tot = sum(t for t, _ in agg.values())
 print(f"{'us/view':>9} {'n':>4} {'share':>6}  kernel")
 for k, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
     print(f"{t / nv:9.2f} {n:4d} {100 * t / tot:5.1f}%  {k}")
-print(f"{tot / nv:9.2f} total us/view-step")
+print(f"{tot / nv:9.2f} total kernel us/view-step")
+s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s0.record()
+for _ in range(steps):
+    tr.step()
+s1.record()
+torch.cuda.synchronize()
+print(f"streams {streams}: {s0.elapsed_time(s1) * 1e3 / nv:9.2f} wall us/view-step")
