@@ -436,8 +436,14 @@ constexpr int kX4CellRows = 8;               // cell rows per tile = warps per C
 constexpr int kX4SpanC = kX4Groups + 2;      // corner columns of a tile
 constexpr int kX4SpanR = kX4CellRows + 1;    // corner rows of a tile
 
+#ifndef UP_TMA_STORE
+#define UP_TMA_STORE 1
+#endif
+#ifndef UP_X4_MINB
+#define UP_X4_MINB 1
+#endif
 template <bool CLAMP>
-__global__ void __launch_bounds__(256) upscale_x4_kernel(const float* __restrict__ src, int in_w, int in_h,
+__global__ void __launch_bounds__(256, UP_X4_MINB) upscale_x4_kernel(const float* __restrict__ src, int in_w, int in_h,
                                                          float* __restrict__ out, int out_w, int out_h) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[2];
@@ -537,6 +543,29 @@ __global__ void __launch_bounds__(256) upscale_x4_kernel(const float* __restrict
                         o[3 * i + c] = CLAMP ? fma_sat(w0, G[ka][c], part) : fmaf(w0, G[ka][c], part);
                     }
                 }
+#if UP_TMA_STORE
+                // the warp's 128 pixels (1536 B) go to shared memory (double-buffered per
+                // warp) and leave as one bulk copy (TMA engine), not 96 LSU stores
+                const int sb_i = j & 1;
+                float4* w4 = s_xp + (warp * 2 + sb_i) * 96;
+                if (lane == 0)   // the bulk copy that last read this buffer has finished reading
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncwarp(active);
+                w4[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
+                w4[3 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
+                w4[3 * lane + 2] = make_float4(o[8], o[9], o[10], o[11]);
+                const int gw = (t % ngx) * kX4Groups;        // first group of this warp row
+                float4* d4 = reinterpret_cast<float4*>(out + ((size_t)v * out_w + 4 * gw) * 3);
+                const int nvalid = 3 * min(kX4Groups, out_w / 4 - gw);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp(active);
+                if (lane == 0) {
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d4),
+                                 "r"(smem_u32(w4)), "r"((uint32_t)nvalid * 16u)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+#else
                 // transpose the warp's 128 pixels (1536 B) through shared memory so each
                 // 16-byte store instruction writes 512 contiguous bytes (whole lines)
                 float4* w4 = s_xp + warp * 96;
@@ -550,10 +579,14 @@ __global__ void __launch_bounds__(256) upscale_x4_kernel(const float* __restrict
                 const int nact = __popc(active);   // active lanes are 0 .. nact-1
                 for (int k = lane; k < nvalid; k += nact) __stcs(d4 + k, w4[k]);
                 __syncwarp(active);
+#endif
             }
         }
         __syncthreads();   // stage b is refilled by the prefetch of the next iteration
     }
+#if UP_TMA_STORE
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
 }
 
 // ---- backward -----------------------------------------------------------------
@@ -894,7 +927,7 @@ static int upscale_int_launch(const float* src, int in_w, int in_h, float* out, 
 template <bool CLAMP>
 static int upscale_x4_launch(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
                              cudaStream_t stream) {
-    const size_t smem = 2 * (size_t)kX4SpanR * kX4SpanC * 48 + 8 * 96 * 16;
+    const size_t smem = 2 * (size_t)kX4SpanR * kX4SpanC * 48 + 8 * 96 * 16 * (UP_TMA_STORE ? 2 : 1);
     static int per_sm = 0, sms = 0;
     if (!per_sm) {
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_x4_kernel<CLAMP>,
