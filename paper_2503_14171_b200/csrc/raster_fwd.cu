@@ -236,11 +236,9 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
     __shared__ PackF s_pack[kWarps][2][32];
     __shared__ float4 s_col[kWarps][2][32];
     __shared__ uint32_t s_rank[kWarps][2][32];
-    __shared__ uint8_t s_list[kWarps][4][32];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = lane >> 3, li = lane & 7;
-    const uint32_t lt = (1u << lane) - 1u;
     const uint32_t nunits = (uint32_t)(p.ntx * ((p.height + kTile - 1) / kTile)) * kRects;
 
     // Persistent, per-warp dynamic scheduling: a warp claims (tile, 8x4 rectangle)
@@ -317,17 +315,17 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
 #endif
                     }
                 }
-                int cnt_my = 0, cnt_max = 0;
+                int cnt_max = 0;
+                uint32_t my_mask = 0;   // this lane's group: candidates of the chunk, walked low to high
 #if RASTER_STATS
                 int cnt_sum = 0;
 #endif
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
                     const uint32_t mq = __ballot_sync(0xffffffffu, (gmask >> qq) & 1u);
-                    if ((gmask >> qq) & 1u) s_list[warp][qq][__popc(mq & lt)] = (uint8_t)lane;
                     const int c = __popc(mq);
                     cnt_max = max(cnt_max, c);
-                    if (qq == q) cnt_my = c;
+                    if (qq == q) my_mask = mq;
 #if RASTER_STATS
                     cnt_sum += c;
 #endif
@@ -343,12 +341,13 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                 for (int k = 0; k < cnt_max; ++k) {
 #if RASTER_STATS
                     {
-                        const uint32_t ev = __ballot_sync(0xffffffffu, active && k < cnt_my);
+                        const uint32_t ev = __ballot_sync(0xffffffffu, active && my_mask != 0u);
                         if (lane == 0) atomicAdd((unsigned long long*)&p.counters[14], (unsigned long long)__popc(ev));
                     }
 #endif
-                    if (active && k < cnt_my) {
-                        const int idx = s_list[warp][q][k];
+                    if (active && my_mask != 0u) {
+                        const int idx = __ffs(my_mask) - 1;
+                        my_mask &= my_mask - 1u;
                         blend_candidate<TRAIN>(p, s_pack[warp][b][idx], s_col[warp][b][idx],
                                                s_rank[warp][b][idx], base + idx, px, py, cx, cy, s, active,
                                                flagged);
