@@ -209,6 +209,9 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 // group.  Step k of the blend loop then advances every group by one of ITS
 // candidates (four candidates per warp instruction stream), which roughly
 // halves the lanes idling on candidates that miss their pixels.
+#ifndef RASTER_NO_WARP_EXACT
+#define RASTER_NO_WARP_EXACT 1
+#endif
 #ifndef RASTER_TERM_MASK
 #define RASTER_TERM_MASK 7
 #endif
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                 uint32_t gmask = 0;   // bit g: candidate reaches group g's 4x2 rectangle
                 if (base + lane < end) {
                     const PackF g = s_pack[warp][b][lane];
-                    if (ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
+                    if (RASTER_NO_WARP_EXACT || ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
 #if RASTER_GROUP_EXACT
                         // groups: the exact ellipse test against each 4x2 rectangle
                         gmask = (ellipse_hits_rect(g, X0, X0 + 3.f, Y0, Y0 + 1.f) ? 1u : 0u) |
