@@ -209,6 +209,9 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 // group.  Step k of the blend loop then advances every group by one of ITS
 // candidates (four candidates per warp instruction stream), which roughly
 // halves the lanes idling on candidates that miss their pixels.
+#ifndef RASTER_PACK_PAD
+#define RASTER_PACK_PAD 1
+#endif
 #ifndef RASTER_NO_WARP_EXACT
 #define RASTER_NO_WARP_EXACT 1
 #endif
@@ -236,7 +239,18 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 template <bool TRAIN>
 __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_kernel(RasterArgs p) {
     // per warp, double-buffered: chunk c+1 is fetched with cp.async (LDGSTS) while chunk c blends
+#if RASTER_PACK_PAD
+    // 80-byte stride: the four groups' candidates of a step fall on different banks
+    struct PackS {
+        PackF f;
+        float4 pad;
+    };
+    __shared__ PackS s_packs[kWarps][2][32];
+#define S_PACK(w, b, i) (s_packs[w][b][i].f)
+#else
     __shared__ PackF s_pack[kWarps][2][32];
+#define S_PACK(w, b, i) (s_pack[w][b][i])
+#endif
     __shared__ float4 s_col[kWarps][2][32];
     __shared__ uint32_t s_rank[kWarps][2][32];
 
@@ -272,7 +286,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
         auto stage = [&](uint32_t cbase, int b, uint32_t r) {
             if (cbase + lane < end) {
                 const float4* src = reinterpret_cast<const float4*>(p.pack + r);
-                float4* dst = reinterpret_cast<float4*>(&s_pack[warp][b][lane]);
+                float4* dst = reinterpret_cast<float4*>(&S_PACK(warp, b, lane));
                 cp_async16(dst, src);
                 cp_async16(dst + 1, src + 1);
                 cp_async16(dst + 2, src + 2);
@@ -298,7 +312,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                 __syncwarp();
                 uint32_t gmask = 0;   // bit g: candidate reaches group g's 4x2 rectangle
                 if (base + lane < end) {
-                    const PackF g = s_pack[warp][b][lane];
+                    const PackF g = S_PACK(warp, b, lane);
                     if (RASTER_NO_WARP_EXACT || ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
 #if RASTER_GROUP_EXACT
                         // groups: the exact ellipse test against each 4x2 rectangle
@@ -351,7 +365,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                     if (active && my_mask != 0u) {
                         const int idx = __ffs(my_mask) - 1;
                         my_mask &= my_mask - 1u;
-                        blend_candidate<TRAIN>(p, s_pack[warp][b][idx], s_col[warp][b][idx],
+                        blend_candidate<TRAIN>(p, S_PACK(warp, b, idx), s_col[warp][b][idx],
                                                s_rank[warp][b][idx], base + idx, px, py, cx, cy, s, active,
                                                flagged);
                     }
