@@ -125,7 +125,10 @@ __device__ __forceinline__ float group_reduce9(const float (&g)[kG], int li, flo
 constexpr int kRing = BWD_GROUPS ? RING_G : 8;
 
 struct BwdShared {
-    PackF pack[kWarps_bw][kBwBatch];
+    struct {
+        PackF f;
+        float4 pad;   // 80-byte stride: the four groups' candidates fall on different banks
+    } pack[kWarps_bw][kBwBatch];
     float4 col[kWarps_bw][kBwBatch];
     uint32_t rank[kWarps_bw][kBwBatch];
     float part[kRing][kWarps_bw][kBwBatch][kG];
@@ -229,14 +232,14 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
             if (work) {
                 const PackF g = p.pack[r];
                 keep = ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f);
-                s_pack[warp][lane] = g;
+                s_pack[warp][lane].f = g;
                 s_col[warp][lane] = p.sc.color[r];
             }
         }
 #if BWD_GROUPS
         uint32_t gmask = 0;   // bit g: candidate reaches group g's 4x2 rectangle
         if (keep) {
-            const PackF& g = s_pack[warp][lane];
+            const PackF& g = s_pack[warp][lane].f;
             const float lx = g.mxh - g.ex, hx = g.mxh + g.ex;
             const float ly = g.myh - g.ey, hy = g.myh + g.ey;
             const uint32_t c0 = (lx <= X0 + 3.f && hx >= X0) ? 1u : 0u;
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
             for (int i = 0; i < kG; ++i) gr[i] = 0.f;
             bool contrib = false;
             if (has && live && lo + idx < my_last) {
-                const PackF g = s_pack[warp][idx];
+                const PackF g = s_pack[warp][idx].f;
                 float al, gax, gay, gaxy, rel;
                 int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
                 if (st == kUnsure) {
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
             for (int i = 0; i < kG; ++i) gr[i] = 0.f;
             bool contrib = false;
             if (live && jk < my_last) {
-                const PackF g = s_pack[warp][k];
+                const PackF g = s_pack[warp][k].f;
                 float al, gax, gay, gaxy, rel;
                 int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
                 if (st == kUnsure) {
