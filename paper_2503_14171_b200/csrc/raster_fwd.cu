@@ -243,15 +243,17 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
     // 80-byte stride: the four groups' candidates of a step fall on different banks
     struct PackS {
         PackF f;
-        float4 pad;
+        float4 col;   // the candidate's colour rides in the fifth 16-byte slot
     };
     __shared__ PackS s_packs[kWarps][2][32];
 #define S_PACK(w, b, i) (s_packs[w][b][i].f)
+#define S_COL(w, b, i) (s_packs[w][b][i].col)
 #else
     __shared__ PackF s_pack[kWarps][2][32];
-#define S_PACK(w, b, i) (s_pack[w][b][i])
-#endif
     __shared__ float4 s_col[kWarps][2][32];
+#define S_PACK(w, b, i) (s_pack[w][b][i])
+#define S_COL(w, b, i) (s_col[w][b][i])
+#endif
     __shared__ uint32_t s_rank[kWarps][2][32];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                 cp_async16(dst + 1, src + 1);
                 cp_async16(dst + 2, src + 2);
                 cp_async16(dst + 3, src + 3);
-                cp_async16(&s_col[warp][b][lane], p.sc.color + r);
+                cp_async16(&S_COL(warp, b, lane), p.sc.color + r);
                 s_rank[warp][b][lane] = r;
             }
             cp_async_commit();
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                     if (active && my_mask != 0u) {
                         const int idx = __ffs(my_mask) - 1;
                         my_mask &= my_mask - 1u;
-                        blend_candidate<TRAIN>(p, S_PACK(warp, b, idx), s_col[warp][b][idx],
+                        blend_candidate<TRAIN>(p, S_PACK(warp, b, idx), S_COL(warp, b, idx),
                                                s_rank[warp][b][idx], base + idx, px, py, cx, cy, s, active,
                                                flagged);
                     }
