@@ -116,9 +116,13 @@ __global__ void preprocess_kernel(SceneConst sc, ViewConst vc, int width, int he
     p.c = (float)c;
     p.sigma = (float)sg;
     p.qcull = (float)q;
-    p.qclamp = (float)log(sg / kAlphaClamp);
-    p.pad0 = (float)(b / a);  // ellipse-rectangle test: edge minimisers (raster_fwd.cu)
-    p.pad1 = (float)(b / c);
+    // ln(sigma / 0.999) in float32 (<= 2 ulp): eval_fast's tolerance carries a qcull-relative
+    // term of 2^-19 qcull >= 16 ulp(qclamp) (qclamp < qcull), so the clamp decision stays certified
+    p.qclamp = logf(p.sigma / (float)kAlphaClamp);
+    // ellipse-rectangle test: edge minimisers (a perturbed minimiser only raises the edge
+    // value by O(eps^2), far inside that test's 2^-18 margin)
+    p.pad0 = p.b / p.a;
+    p.pad1 = p.b / p.c;
     // cull-ellipse half extents (the reference's rx, ry) with a 1e-3 px + 1e-5 relative
     // margin: every pixel centre that can contribute lies in mean +- (ex, ey)
     p.ex = (float)(rx * (1.0 + 1e-5) + 1e-3);
