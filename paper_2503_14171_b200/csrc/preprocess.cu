@@ -380,6 +380,39 @@ __device__ __forceinline__ short4 bin_box(int64_t n, int64_t r, const short4* bb
     return bb;
 }
 
+// One CTA (1024 threads): per tile, exclusive prefix over the group sums (in
+// place) and the tile total, then the exclusive scan of the totals into each
+// list's start (and the pair count) — what colscan_groups_kernel plus a
+// multi-kernel device scan did, in one launch (grids up to kScanTilesMax tiles).
+constexpr int kScanTilesMax = 16384;
+__global__ void __launch_bounds__(1024) colscan_groups_scan_kernel(int ntiles, int ngroups, uint32_t* __restrict__ part,
+                                                                   uint32_t* __restrict__ tile_count,
+                                                                   uint32_t* __restrict__ tile_start,
+                                                                   uint32_t* __restrict__ counters) {
+    extern __shared__ uint32_t s_cnt[];
+    __shared__ uint32_t wsum[33];
+    if (threadIdx.x == 0) counters[5] = 0;
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+        uint32_t run = 0;
+        for (int g0 = 0; g0 < ngroups; g0 += 16) {   // 16 loads in flight, then the prefix
+            uint32_t v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = g0 + i < ngroups ? part[(size_t)(g0 + i) * ntiles + t] : 0u;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (g0 + i < ngroups) part[(size_t)(g0 + i) * ntiles + t] = run;
+                run += v[i];
+            }
+        }
+        tile_count[t] = run;
+        s_cnt[t] = run;
+    }
+    __syncthreads();
+    const uint32_t total = block_exclusive_scan(s_cnt, ntiles, wsum);
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) tile_start[t] = s_cnt[t];
+    if (threadIdx.x == 0) counters[0] = total;
+}
+
 __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
     int64_t n, const short4* __restrict__ bboxes, const uint32_t* __restrict__ touched, int ntx, int ntiles,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ part, const uint32_t* __restrict__ tile_start,
@@ -833,6 +866,8 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
                                                   kBinSmemMax));
             SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fill_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   kBinSmemMax));
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(colscan_groups_scan_kernel,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kScanTilesMax * 4));
             configured = true;
         }
         uint32_t* hist = (uint32_t*)(ws + L.bin_hist);
@@ -843,10 +878,16 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         colscan_rows_kernel<<<dim3(ceil_div(ntiles, 128), ngroups), 128, 0, stream>>>(ntiles, (int)nrows, hist,
                                                                                      part);
         note_launch();
-        colscan_groups_kernel<<<ceil_div(ntiles, 128), 128, 0, stream>>>(ntiles, ngroups, part, tile_count,
-                                                                        counters);
-        note_launch();
-        exclusive_scan_u32(tile_count, tile_start, ntiles, scan_tmp, &counters[0], stream);
+        if (ntiles <= kScanTilesMax) {
+            colscan_groups_scan_kernel<<<1, 1024, ntiles * 4, stream>>>(ntiles, ngroups, part, tile_count,
+                                                                        tile_start, counters);
+            note_launch();
+        } else {
+            colscan_groups_kernel<<<ceil_div(ntiles, 128), 128, 0, stream>>>(ntiles, ngroups, part, tile_count,
+                                                                            counters);
+            note_launch();
+            exclusive_scan_u32(tile_count, tile_start, ntiles, scan_tmp, &counters[0], stream);
+        }
         fill_rows_kernel<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, part,
                                                                   tile_start, tile_count, ranges, L.cap, ranks,
                                                                   keys, counters, (const uint32_t*)(ws + L.offsets),
