@@ -50,6 +50,16 @@ typedef struct {
     const double *depths;         /* (n)   */
 } splat_scene_t;
 
+/* Pinhole camera for the 3D front-end: world -> camera
+ * x_c = R x_w + t (R row-major), pixel = (fx x/z + cx, fy y/z + cy) on the
+ * camera image, points with z <= near_plane are culled. */
+typedef struct {
+    double R[9];
+    double t[3];
+    double fx, fy, cx, cy;
+    double near_plane;
+} splat_camera_t;
+
 /* One camera view (host values).  The render of view v at W x H equals the
  * reference render_forward of Scene(means - (ox, oy), ..., reference_resolution
  * = (W/kx_ratio...)) with kx = out_w / ref_w, ky = out_h / ref_h exactly as
@@ -168,6 +178,17 @@ int splat_loss(const float *pred, const float *target, int width, int height, do
  * moments, float32 gradients; bc1/bc2 = 1 - beta^t computed by the caller. */
 int splat_adam_step(double *params, const float *grads, double *m, double *v, int64_t count, double lr,
                     double beta1, double beta2, double bc1, double bc2, double eps, void *stream);
+
+/* 3D EWA front-end: n 3D Gaussians (means (n,3), log_scales
+ * (n,3), quaternions (n,4) w,x,y,z, opacity logits (n)) seen by `camera` ->
+ * the 2D scene arrays (means (n,2) in camera-image pixels, log_scales (n,2),
+ * rotations (n), opacity logits (n; -100 behind the near plane), depths (n) =
+ * camera z) in the reference's 2D parametrisation (core.py:175-182), float64.
+ * The colours pass through unchanged. */
+int splat_project_3d(int64_t n, const double *means3, const double *log_scales3, const double *quats,
+                     const double *opacity_logits, const splat_camera_t *camera, double *means2,
+                     double *log_scales2, double *rotations, double *opacity_logits_out, double *depths,
+                     void *stream);
 
 /* dst += src over `count` floats: folds per-stream gradient buffers (views
  * rendered concurrently) into one in a fixed order (deterministic sum of the

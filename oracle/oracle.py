@@ -574,3 +574,48 @@ def adam_step(params: dict, grads: dict, m: dict, v: dict, t: int, lrs: dict,
         v[k] = beta2 * v[k] + (1.0 - beta2) * g * g
         out[k] = p - lrs[k] * (m[k] / bc1) / (np.sqrt(v[k] / bc2) + eps)
     return out, m, v, t
+
+
+# ---- 3D front-end ---------------------------------------
+
+def project_gaussians(means3, log_scales3, quats, opacity_logits, R, t, fx, fy, cx, cy, near):
+    """float64 restatement of the EWA local-affine projection (PAPER.md:154-162:
+    Sigma' = J W Sigma W^T J^T) into the reference's 2D parametrisation
+    (core.py:175-182).  The reference package is 2D-only, so this restatement is
+    the pin for csrc/project.cu ("parity unpinned" w.r.t. the reference itself).
+    Returns (means2 (N,2), log_scales2 (N,2), rotations (N,), opacity_logits (N,), depths (N,))."""
+    mu = np.asarray(means3, np.float64).reshape(-1, 3)
+    R = np.asarray(R, np.float64).reshape(3, 3)
+    t = np.asarray(t, np.float64).reshape(3)
+    cam = mu @ R.T + t
+    x, y, z = cam[:, 0], cam[:, 1], cam[:, 2]
+    ok = z > near
+    zs = np.where(ok, z, 1.0)
+    q = np.asarray(quats, np.float64).reshape(-1, 4)
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w_, a_, b_, c_ = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+    Q = np.stack([
+        np.stack([1 - 2 * (b_ * b_ + c_ * c_), 2 * (a_ * b_ - w_ * c_), 2 * (a_ * c_ + w_ * b_)], -1),
+        np.stack([2 * (a_ * b_ + w_ * c_), 1 - 2 * (a_ * a_ + c_ * c_), 2 * (b_ * c_ - w_ * a_)], -1),
+        np.stack([2 * (a_ * c_ - w_ * b_), 2 * (b_ * c_ + w_ * a_), 1 - 2 * (a_ * a_ + b_ * b_)], -1)], 1)
+    s2 = np.exp(2.0 * np.asarray(log_scales3, np.float64).reshape(-1, 3))
+    J = np.zeros((len(mu), 2, 3))
+    J[:, 0, 0] = fx / zs
+    J[:, 0, 2] = -fx * x / (zs * zs)
+    J[:, 1, 1] = fy / zs
+    J[:, 1, 2] = -fy * y / (zs * zs)
+    M = J @ R @ Q                                        # (N, 2, 3)
+    S = np.einsum("nik,nk,njk->nij", M, s2, M)           # M diag(s2) M^T
+    a, b, c = S[:, 0, 0], S[:, 0, 1], S[:, 1, 1]
+    h = 0.5 * (a + c)
+    d = np.sqrt(0.25 * (a - c) ** 2 + b * b)
+    lmax = h + d
+    lmin = np.maximum(h - d, 1e-12 * lmax)
+    means2 = np.stack([fx * x / zs + cx, fy * y / zs + cy], 1)
+    ls2 = np.stack([0.5 * np.log(lmax), 0.5 * np.log(lmin)], 1)
+    rot = 0.5 * np.arctan2(2.0 * b, a - c)
+    logits = np.where(ok, np.asarray(opacity_logits, np.float64).reshape(-1), -100.0)
+    means2[~ok] = (cx, cy)
+    ls2[~ok] = 0.0
+    rot[~ok] = 0.0
+    return means2, ls2, rot, logits, z

@@ -38,6 +38,10 @@ class ViewT(ctypes.Structure):
     _fields_ = [("kx", D), ("ky", D), ("ox", D), ("oy", D), ("bg", D * 3)]
 
 
+class CameraT(ctypes.Structure):
+    _fields_ = [("R", D * 9), ("t", D * 3), ("fx", D), ("fy", D), ("cx", D), ("cy", D), ("near_plane", D)]
+
+
 class GimgT(ctypes.Structure):
     _fields_ = [("planes", P), ("alpha", P), ("count", P), ("last", P), ("state", P)]
 
@@ -67,6 +71,7 @@ SIGNATURES = {
     "splat_gimg_unpack": (I32, [P, I32, I32, P, P, P, P]),
     "splat_encode_display": (I32, [P, I64, P, P]),
     "splat_grad_accumulate": (I32, [P, P, I64, P]),
+    "splat_project_3d": (I32, [I64, P, P, P, P, ctypes.POINTER(CameraT), P, P, P, P, P, P]),
     "splat_rasterize": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
                               ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_view_pack64": (I32, [P, I64, ctypes.POINTER(ViewT), P, P]),

@@ -49,6 +49,9 @@ int gimg_unpack_impl(const float* in, int w, int h, float* planes, float* alpha,
                      cudaStream_t stream);
 int encode_display_impl(const float* img, int64_t n, uint8_t* out, cudaStream_t stream);
 int accumulate_impl(float* dst, const float* src, int64_t n, cudaStream_t stream);
+int project_impl(int64_t n, const double* mu, const double* ls3, const double* quat, const double* logit,
+                 const splat_camera_t& cam, double* means2, double* ls2, double* rot2, double* logit_out,
+                 double* depth, cudaStream_t stream);
 
 static int check_dims(int width, int height) {
     if (width <= 0 || height <= 0)
@@ -255,6 +258,18 @@ int splat_gimg_unpack(const float* in, int width, int height, float* planes, flo
                       void* stream) {
     if (width <= 0 || height <= 0) return set_error(SPLAT_ERR_DIMENSION, "image dimensions must be positive");
     return gimg_unpack_impl(in, width, height, planes, alpha, count, (cudaStream_t)stream);
+}
+
+int splat_project_3d(int64_t n, const double* means3, const double* log_scales3, const double* quats,
+                     const double* opacity_logits, const splat_camera_t* camera, double* means2,
+                     double* log_scales2, double* rotations, double* opacity_logits_out, double* depths,
+                     void* stream) {
+    if (n < 0) return set_error(SPLAT_ERR_DIMENSION, "negative splat count");
+    if (!camera) return set_error(SPLAT_ERR_PARAMETER, "camera is required");
+    if (!(camera->fx > 0.0) || !(camera->fy > 0.0) || !(camera->near_plane > 0.0))
+        return set_error(SPLAT_ERR_PARAMETER, "camera focal lengths and near plane must be positive");
+    return project_impl(n, means3, log_scales3, quats, opacity_logits, *camera, means2, log_scales2, rotations,
+                        opacity_logits_out, depths, (cudaStream_t)stream);
 }
 
 int splat_grad_accumulate(float* dst, const float* src, int64_t count, void* stream) {
