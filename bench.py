@@ -471,6 +471,11 @@ def main():
         traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
         pass
+    util = {}
+    try:
+        util = json.load(open(os.path.join(ROOT, "profiles", "ncu_util.json")))
+    except Exception:
+        pass
     roof = None
     roof_up = None
     if stage:
@@ -482,7 +487,10 @@ def main():
                 "traffic": traffic.get("raster_fwd_kernel"),
                 "algorithmic": {"flops_per_view": raster_flops, "K_contrib_per_view": K,
                                 "E_bbox_evals_per_view": E, "formula": "27P + 13E + 69K (SURVEY 8d)"},
-                "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (median SM clock in run)"}
+                "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (median SM clock in run)",
+                "ncu_utilisation": util.get("raster_fwd_kernel"),
+                "note": "the SURVEY 8(d) FLOP count omits the certified-decision arithmetic, culling and "
+                        "blend bookkeeping; the kernel is issue-bound (see ncu_utilisation)"}
         u_ms = stage["upscale"]
         roof_up = {"kernel": "upscale_x4_kernel" if F == 4.0 else "upscale_int_kernel<2>", "bound": "hbm",
                    "measured": f"CUDA events per stage, single-stream pass over {len(kviews)} views",
