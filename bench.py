@@ -304,12 +304,57 @@ def run_train(args):
         tcpu = cpu_reference_train_view(model, tgt0, mine[0], c)
         cpu = {"value": 1.0 / tcpu, "unit": "view-steps/s", "cores": O.default_threads(), "kind": "port",
                "sample": "1 C5 view-step (fwd, x4 upscale, L1+SSIM, upscale bwd, raster bwd) through the oracle"}
+    # roofline of the dominant kernel (the rasterizer backward): one view at a time on one
+    # stream, CUDA events around render_backward, algorithmic FLOPs per SURVEY 8(d)
+    roof = None
+    if rank == 0:
+        from paper_2503_14171_b200.raster_backward import PixelAdjoint, render_backward
+        from paper_2503_14171_b200.spline import upscale_backward, upscale_spline
+        tr_ds = trainer.ds
+        tms, flops = 0.0, 0.0
+        for v, tgt in zip(mine, targets):
+            fwd = render_forward(tr_ds, c.width, c.height, view=v, train=True)
+            pred = upscale_spline(fwd, 1.0, out_size=(W, H))
+            _, adj_img = fit.loss_device(pred, tgt, 0.2)
+            adj = PixelAdjoint.from_source(upscale_backward(fwd, 1.0, adj_img, out_size=(W, H)))
+            K = float(fwd.contrib_count.sum(dtype=torch.int64))
+            bb = fwd.frame.bboxes().to(torch.int64)
+            E = float(((bb[:, 1] - bb[:, 0]) * (bb[:, 3] - bb[:, 2]))[fwd.frame.touched() > 0].sum())
+            gbuf = trainer.grads   # scratch use after the timed steps
+            render_backward(tr_ds, fwd, adj, out=gbuf, check_finite=False)   # warm (workspace allocation)
+            # the same ABI call with its arguments prepared, so the events bracket device work only
+            fr = fwd.frame
+            nb = lib.splat_backward_workspace_bytes(tr_ds.n, fr.capacity)
+            bws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            cargs = (_lib.ptr(tr_ds.const), tr_ds.c_scene(), fwd.view, c.width, c.height, fwd.c_gimg(),
+                     _lib.ptr(adj.planes), _lib.ptr(fr.ws), fr.nbytes, fr.capacity, _lib.ptr(bws), nb,
+                     _lib.ptr(gbuf.flat), 0, _lib.stream_ptr())
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _lib.check(lib.splat_render_backward(*cargs))
+            e1.record()
+            torch.cuda.synchronize()
+            tms += e0.elapsed_time(e1)
+            flops += c.width * c.height * 27.0 + 13.0 * E + 360.0 * K
+        sm_mhz = (clk or {}).get("sm_mhz") or 1335.0
+        peak = NUM_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+        ach = flops / (tms * 1e-3) / 1e12
+        roof = {"kernel": "raster_bwd_kernel + reduce_pairs_kernel + chain_kernel (splat_render_backward, per view)",
+                "bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "measured": f"CUDA events around the splat_render_backward call, {len(mine)} views one at a time",
+                "algorithmic": {"formula": "27P + 13E + 360K (SURVEY 8d backward; E = bbox-tested upper bound)",
+                                "flops_per_view": flops / len(mine)},
+                "traffic": json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("raster_bwd_kernel")
+                if os.path.exists(os.path.join(ROOT, "profiles", "ncu_traffic.json")) else None,
+                "ms_per_view": tms / len(mine)}
     if rank == 0:
         line = {"metric": TRAIN_METRIC, "value": value, "unit": "view-steps/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": train_config(c, world, vpr), "gpu_launches": int(launches),
                 "loss_last_step": [float(x) for x in losses[:, 0]],
+                "roofline": roof,
                 "cpu_baseline": cpu,
                 "e2e": {"value": total_views / (ems / 1e3), "unit": "view-steps/s", "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(vals.numel() * 8), "steps": ksteps},
