@@ -8,9 +8,10 @@
 //                    (raster_forward.py:79-123) with the reference's float64
 //                    expression trees and explicitly rounded (non-fused) ops, so
 //                    the integer bboxes and validity are bit-identical.
-//   emit + sort    : duplicate (tile, rank) pairs in rank order, stable radix
-//                    sort on the tile bits, per-tile [start, end) ranges
-//                    (bin_tiles, raster_forward.py:136-149).
+//   binning      : per-4096-rank-block tile histograms, column scan, staged
+//                    counting-sort fill -> per-tile lists in the reference's
+//                    append order and [start, end) ranges (bin_tiles,
+//                    raster_forward.py:136-149); see "tile binning" below.
 #include <cmath>
 
 #include "kernels.cuh"
@@ -132,74 +133,7 @@ __global__ void preprocess_kernel(SceneConst sc, ViewConst vc, int width, int he
     pack[r] = p;
 }
 
-// Pair emission, warp-cooperative: the 32 ranks of a warp own the contiguous
-// slot range [offsets[r0], offsets[r0+32]); lane l writes slots l, l+32, ...
-// (coalesced) after a 5-step shuffle binary search for the slot's owner rank.
-// Pairs of one rank are written in row-major tile order, ranks ascending
-// (raster_forward.py:141-148 append order).
-__global__ void emit_pairs_kernel(int64_t n, const short4* __restrict__ bboxes,
-                                  const uint32_t* __restrict__ touched,
-                                  const uint32_t* __restrict__ offsets, int ntx, int64_t cap,
-                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ ranks,
-                                  uint32_t* __restrict__ counters) {
-    const int lane = threadIdx.x & 31;
-    const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
-    if (r0 >= n) return;
-    const int64_t r = r0 + lane;
-    const bool have = r < n;
-    const uint32_t cnt = have ? touched[r] : 0u;
-    const uint32_t off = have ? offsets[r] : 0u;
-    const uint32_t off0 = __shfl_sync(0xffffffffu, off, 0);
-    const uint32_t incl = (have ? off - off0 : 0u) + cnt;          // inclusive end of this lane's slots
-    uint32_t warp_total = incl;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) warp_total = max(warp_total, __shfl_xor_sync(0xffffffffu, warp_total, d));
-    const uint32_t key = have ? incl : 0xffffffffu;                // monotone search key
-    int tx0 = 0, ty0 = 0, nx = 1;
-    if (cnt) {
-        const short4 bb = bboxes[r];
-        tx0 = bb.x / kTile;
-        ty0 = bb.z / kTile;
-        nx = (bb.y - 1) / kTile - tx0 + 1;
-    }
-    if ((int64_t)off0 + warp_total > cap && lane == 0) {
-        atomicOr(&counters[1], 1u);
-        atomicOr(&counters[4], 1u);  // sticky until the caller clears it
-    }
-    for (uint32_t sb = 0; sb < warp_total; sb += 32) {   // uniform trip count: full-warp shuffles
-        const uint32_t s = sb + lane;
-        // owner = first lane whose inclusive end exceeds s
-        int lo = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const uint32_t e = __shfl_sync(0xffffffffu, key, lo + step - 1);
-            if (e <= s) lo += step;
-        }
-        const uint32_t start = __shfl_sync(0xffffffffu, incl - cnt, lo);
-        const int otx0 = __shfl_sync(0xffffffffu, tx0, lo);
-        const int oty0 = __shfl_sync(0xffffffffu, ty0, lo);
-        const int onx = __shfl_sync(0xffffffffu, nx, lo);
-        const int64_t slot = (int64_t)off0 + s;
-        if (s < warp_total && slot < cap) {
-            const uint32_t li = s - start;
-            const int ty = oty0 + (int)(li / (uint32_t)onx), tx = otx0 + (int)(li % (uint32_t)onx);
-            keys[slot] = (uint32_t)(ty * ntx + tx);
-            ranks[slot] = (uint32_t)(r0 + lo);
-        }
-    }
-}
 
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const uint32_t* counters,
-                                   int64_t cap, int ntiles, uint32_t* __restrict__ ranges) {
-    int64_t np = counters[0];
-    if (np > cap) np = cap;
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= np) return;
-    uint32_t k = keys[j];
-    if (k >= (uint32_t)ntiles) return;  // defensive: never index past the range table
-    if (j == 0 || keys[j - 1] != k) ranges[2 * k] = (uint32_t)j;
-    if (j == np - 1 || keys[j + 1] != k) ranges[2 * k + 1] = (uint32_t)(j + 1);
-}
 
 __global__ void pack64_kernel(SceneConst sc, ViewConst vc, double* __restrict__ out) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -672,11 +606,6 @@ __global__ void __launch_bounds__(kSegThreadsLarge) segsort_large_kernel(const u
     }
 }
 
-int tile_key_bits(int ntiles) {
-    int bits = 0;
-    while ((1 << bits) < ntiles) ++bits;
-    return bits == 0 ? 1 : bits;
-}
 
 }  // namespace
 
