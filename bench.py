@@ -283,16 +283,29 @@ def run_train(args):
     ms = D.max_over_ranks(s0.elapsed_time(s1) / args.steps, device="cuda")
     total_views = D.total_items(len(mine), device="cuda")
     value = total_views / (ms / 1e3)
-    # e2e: targets streamed from pinned host memory every step, losses read back
+    # e2e: every step's targets streamed from pinned host memory (uploaded one step ahead on a
+    # copy stream, overlapping the previous step), losses read back every step
     host_t = [t.cpu().pin_memory() for t in targets]
     h2d = sum(t.numel() * t.element_size() for t in host_t)
+    ksteps = max(1, min(args.steps, 5))
+    # per-step losses come back through a pinned double buffer: step k's read completes
+    # while step k+1 is already queued, so the host never starves the device
+    lbuf = [torch.empty_like(trainer.values, device="cpu").pin_memory() for _ in range(2)]
+    lev = [torch.cuda.Event() for _ in range(2)]
+    torch.cuda.synchronize()
     e0 = time.perf_counter()
-    ksteps = max(1, min(args.steps, 3))
-    for _ in range(ksteps):
-        for i, t in enumerate(host_t):
-            trainer.targets[i].copy_(t, non_blocking=True)
+    trainer.prefetch_targets(host_t)
+    for k in range(ksteps):
         vals = trainer.step()
-        losses = vals.cpu()
+        if k + 1 < ksteps:
+            trainer.prefetch_targets(host_t)
+        lbuf[k % 2].copy_(vals, non_blocking=True)
+        lev[k % 2].record()
+        if k > 0:
+            lev[(k - 1) % 2].synchronize()
+            losses = lbuf[(k - 1) % 2].clone()
+    lev[(ksteps - 1) % 2].synchronize()
+    losses = lbuf[(ksteps - 1) % 2].clone()
     torch.cuda.synchronize()
     ems = D.max_over_ranks((time.perf_counter() - e0) / ksteps * 1e3, device="cuda")
     clk = clocks.stop()

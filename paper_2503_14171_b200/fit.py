@@ -165,6 +165,27 @@ class ViewTrainer:
         self._adjs = [torch.empty((h, w, 3), dtype=torch.float32, device=self.ds.device)
                       for _ in range(self.streams)]
         self._calibrate()
+        self._copy_stream = None
+        self._staged = None      # (targets, event) uploaded ahead of the next step
+
+    def prefetch_targets(self, host_targets) -> None:
+        """Upload the next step's targets (pinned host tensors) on a copy stream,
+        into a second buffer set, so the PCIe transfer overlaps the current step.
+        The next :meth:`step` waits for the copies and swaps the buffers in."""
+        dev = self.ds.device
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(device=dev)
+            self._spare = [torch.empty_like(t) for t in self.targets]
+            self._spare_free = torch.cuda.Event()
+            self._spare_free.record(torch.cuda.current_stream(dev))
+        cs = self._copy_stream
+        cs.wait_event(self._spare_free)          # the step that last read these buffers is done
+        with torch.cuda.stream(cs):
+            for dst, src in zip(self._spare, host_targets):
+                dst.copy_(src, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        self._staged = (self._spare, ev)
 
     def _calibrate(self):
         """Size the pair buffers once (host-synchronous), with headroom for the
@@ -196,6 +217,13 @@ class ViewTrainer:
         stream order, so the sum is deterministic for a fixed ``streams``."""
         ds, (rw, rh), (w, h) = self.ds, self.render_size, self.out_size
         main = torch.cuda.current_stream(ds.device)
+        if self._staged is not None:            # targets prefetched by prefetch_targets()
+            spare, ev = self._staged
+            main.wait_event(ev)
+            self._spare, self.targets = self.targets, spare
+            self._staged = None
+            # the old buffers were last read by the previous step, which precedes this point
+            self._spare_free.record(main)
         for st in self._streams:
             st.wait_stream(main)
         self._frames = []

@@ -112,3 +112,25 @@ def test_bicubic_fd_training_step_matches_oracle(P, oracle):
     for f in FIELDS:
         assert rel_err(got[f], ref[f]) < 1e-3, f
     assert any(not torch.equal(before[k], v) for k, v in fit.scene_params(tr.ds).items())
+
+
+def test_prefetched_targets_give_the_same_steps(P):
+    """ViewTrainer.prefetch_targets (double-buffered upload on a copy stream) is
+    bitwise the same training as targets resident on the device."""
+    import torch
+    from paper_2503_14171_b200 import fit
+    from paper_2503_14171_b200.scenes import random_views, synthetic_scene
+    model = synthetic_scene(3000, 96, 64, (1.0, 3.0), seed=5)
+    tsc = synthetic_scene(3000, 96, 64, (1.0, 3.0), seed=7)
+    views = random_views(3, 96, 64, seed=2)
+    tg = [P.render_forward(tsc, 96, 64, view=v).color.clamp(0, 1).contiguous() for v in views]
+    a = fit.ViewTrainer(model.copy(), (24, 16), (96, 64), views, [t.clone() for t in tg])
+    b = fit.ViewTrainer(model.copy(), (24, 16), (96, 64), views, [torch.zeros_like(t) for t in tg])
+    host = [t.cpu().pin_memory() for t in tg]
+    for _ in range(3):
+        va = a.step().clone()
+        b.prefetch_targets(host)
+        vb = b.step().clone()
+        assert torch.equal(va, vb)
+    for k in fit.scene_params(a.ds):
+        assert torch.equal(fit.scene_params(a.ds)[k], fit.scene_params(b.ds)[k]), k
