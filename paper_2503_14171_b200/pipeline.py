@@ -78,11 +78,13 @@ class ViewPipeline:
         """Record CUDA events around every stage (single-slot pipelines only)."""
         self.stage_events = [] if enabled else None
 
-    def render(self, views, host_out=None, keep=False):
+    def render(self, views, host_out=None, keep=False, out=None):
         """Launch every view; returns the list of device outputs if keep (else None).
 
         host_out: optional list of pinned host tensors (ring); frame i is copied
         into host_out[i % len(host_out)] on a side stream, overlapped with rendering.
+        out: optional (V, Ho, Wo, 3) float32 device tensor; view i is upscaled
+        straight into out[i] (the batched layout, no extra copy).
         """
         lib, ds = self.lib, self.scene
         kept = [] if keep else None
@@ -94,8 +96,12 @@ class ViewPipeline:
             st = _lib.stream_ptr(slot.stream)
             k = slot.flip
             slot.flip ^= 1
-            out = slot.out[k] if not keep else torch.empty((self.out_h, self.out_w, 3), dtype=torch.float32,
-                                                            device=ds.device)
+            if out is not None:
+                dst = out[i]
+            elif keep:
+                dst = torch.empty((self.out_h, self.out_w, 3), dtype=torch.float32, device=ds.device)
+            else:
+                dst = slot.out[k]
             if slot.copied[k] is not None:
                 slot.stream.wait_event(slot.copied[k])
             ev = self.stage_events
@@ -116,7 +122,7 @@ class ViewPipeline:
             if ev is not None:
                 marks[3].record(slot.stream)
             _lib.check(lib.splat_upscale_forward(_lib.ptr(slot.img.planes), self.width, self.height,
-                                                 _lib.ptr(out), self.out_w, self.out_h, 1,
+                                                 _lib.ptr(dst), self.out_w, self.out_h, 1,
                                                  _lib.ptr(self.plan), st))
             if ev is not None:
                 marks[4].record(slot.stream)
@@ -126,12 +132,12 @@ class ViewPipeline:
                 done.record(slot.stream)
                 self.copy_stream.wait_event(done)
                 with torch.cuda.stream(self.copy_stream):
-                    host_out[i % len(host_out)].copy_(out, non_blocking=True)
+                    host_out[i % len(host_out)].copy_(dst, non_blocking=True)
                 cp = torch.cuda.Event()
                 cp.record(self.copy_stream)
                 slot.copied[k] = cp
             if keep:
-                kept.append(out)
+                kept.append(dst)
         return kept
 
     def join(self, stream=None):
@@ -175,3 +181,17 @@ class ViewPipeline:
                 tot[j] += marks[j].elapsed_time(marks[j + 1])
         n = len(self.stage_events)
         return {s: t / n for s, t in zip(STAGES, tot)}
+
+
+def render_upscale_views(scene, width: int, height: int, views, *, factor: float = 4.0, out_size=None,
+                         slots: int = 4) -> torch.Tensor:
+    """Batched variant of ``upscale_spline(render_forward(scene, W, H, view=v), factor)``
+    for every view: returns a (V, Ho, Wo, 3) float32 device tensor."""
+    pipe = ViewPipeline(scene, width, height, factor=factor, out_size=out_size, slots=slots,
+                        views_for_capacity=list(views))
+    out = torch.empty((len(views), pipe.out_h, pipe.out_w, 3), dtype=torch.float32, device=pipe.scene.device)
+    pipe.fork()
+    pipe.render(list(views), out=out)
+    pipe.join()
+    pipe.check()
+    return out

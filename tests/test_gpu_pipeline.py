@@ -49,3 +49,16 @@ def test_pipeline_overflow_is_detected():
     torch.cuda.synchronize()
     with pytest.raises(RuntimeError):
         pipe.check()
+
+
+def test_batched_views_api():
+    """render_upscale_views: (V, Ho, Wo, 3) batch == per-view reference API."""
+    import torch
+    import paper_2503_14171_b200 as P
+    from paper_2503_14171_b200.pipeline import render_upscale_views
+    sc = P.synthetic_scene(8000, 128, 72, (0.5, 2.5), seed=4)
+    views = P.random_views(6, 128, 72, seed=5)
+    out = render_upscale_views(sc, 128, 72, views, factor=2.0, slots=3)
+    assert tuple(out.shape) == (6, 144, 256, 3)
+    for i, v in enumerate(views):
+        assert torch.equal(out[i], P.upscale_spline(P.render_forward(sc, 128, 72, view=v), 2.0))
