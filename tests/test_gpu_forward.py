@@ -207,3 +207,13 @@ def test_fd_gradients_match_golden(P):
         dim=2).float().cuda())
     back = P.fd_gradients_backward(adj).double().cpu().numpy()
     assert np.abs(back - g["back"]).max() < 1e-5
+
+
+def test_large_canvas_matches_oracle(P, oracle):
+    """A 2560x2400 render (24,000 tiles: beyond the shared-memory binning tables,
+    so the large-grid binning path runs) stays exact."""
+    from paper_2503_14171_b200.scenes import synthetic_scene
+    sc = synthetic_scene(6000, 2560, 2400, (2.0, 12.0), seed=8)
+    img = P.render_forward(sc, 2560, 2400)
+    ref = oracle.render_forward(sc, 2560, 2400)
+    assert_forward_matches(img.numpy(), {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)}, "large")
