@@ -33,8 +33,8 @@ struct SceneConst {
 
 // Per-view float32 pack the rasterizer consumes (rank order, 64 bytes).
 struct __align__(16) PackF {
-    float mxh, mxl, myh, myl;     // render-space mean as float hi + lo parts
-    float a, b, c, sigma;         // conic and opacity
+    float mxh, myh, mxl, myl;     // render-space mean as float hi + lo parts ((x, y) pairs for FADD2)
+    float a, c, b, sigma;         // conic (a, c adjacent for FMUL2) and opacity
     float qcull, qclamp, pad0, pad1;  // ln(255 sigma), ln(sigma / 0.999), b/a, b/c
     float ex, ey, pad2, pad3;     // half extents of the cull ellipse, padded (pre-filter only)
 };

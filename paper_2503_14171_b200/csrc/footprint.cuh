@@ -5,6 +5,7 @@
 // decisions and values bit for bit).
 #pragma once
 #include <cmath>
+#include <cstring>
 
 #include "kernels.cuh"
 
@@ -69,15 +70,45 @@ __device__ __forceinline__ float fast_rcp(float x) {
 // reference's tests with margin, kUnsure otherwise.  `al` etc. are the
 // canonical float32 values used for blending (identical in the backward pass);
 // `rel` receives the relative error bound of `al`.
+__device__ __forceinline__ uint64_t f2_bits(float2 v) {
+    uint64_t r;
+    memcpy(&r, &v, 8);
+    return r;
+}
+__device__ __forceinline__ float2 bits_f2(uint64_t r) {
+    float2 v;
+    memcpy(&v, &r, 8);
+    return v;
+}
+// Packed float32x2 arithmetic (sm_100 FADD2 / FMUL2 / FFMA2): two IEEE ops per instruction.
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return bits_f2(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return bits_f2(r);
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+    return bits_f2(r);
+}
+
 __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, float& al, float& ax,
                                          float& ay, float& axy, float& rel) {
-    float dx = (cx - g.mxh) - g.mxl;
-    float dy = (cy - g.myh) - g.myl;
-    float adx = g.a * dx;
+    // (dx, dy) = ((cx, cy) - (mxh, myh)) - (mxl, myl), and (a dx, c dy) as packed pairs
+    const float2 d = fsub2(fsub2(make_float2(cx, cy), make_float2(g.mxh, g.myh)), make_float2(g.mxl, g.myl));
+    const float dx = d.x, dy = d.y;
+    const float2 acd = fmul2(make_float2(g.a, g.c), d);
+    const float adx = acd.x;
     float b2 = 2.f * g.b;
-    float t1 = adx * dx;
+    const float2 t13 = fmul2(acd, d);   // (a dx dx, c dy dy)
+    float t1 = t13.x;
     float t2 = (b2 * dx) * dy;
-    float t3 = (g.c * dy) * dy;
+    float t3 = t13.y;
     float qf = (t1 + t2) + t3;
     float s = (t1 + fabsf(t2)) + t3;
     // |qf - Q_exact| <= ~8 ulp * s; conic/mean rounding adds ~4 ulp * s.  2^-19 * s is a 2x margin.
@@ -97,11 +128,12 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
         return kUnsure;
     }
     al = g.sigma * fast_exp2(-1.44269504f * qf);
-    float gx = -2.f * fmaf(g.b, dy, adx);
-    float gy = -2.f * fmaf(g.b, dx, g.c * dy);
-    ax = al * gx;
-    ay = al * gy;
-    axy = al * fmaf(gx, gy, -b2);
+    // (gx, gy) = -2 ((b dy, b dx) + (a dx, c dy))
+    const float2 gxy = fmul2(ffma2(make_float2(g.b, g.b), make_float2(dy, dx), acd), make_float2(-2.f, -2.f));
+    const float2 axy2 = fmul2(make_float2(al, al), gxy);
+    ax = axy2.x;
+    ay = axy2.y;
+    axy = al * fmaf(gxy.x, gxy.y, -b2);
     return kContrib;
 }
 

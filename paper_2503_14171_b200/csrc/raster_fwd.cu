@@ -18,6 +18,8 @@
 // contributor list) therefore equal the reference's; values are float32.
 #include <cmath>
 
+#include <cstring>
+
 #include "footprint.cuh"
 
 namespace splat {
@@ -40,6 +42,10 @@ struct RasterArgs {
     uint32_t* fixup;
     uint32_t* counters;
 };
+
+#ifndef RASTER_FFMA2
+#define RASTER_FFMA2 1
+#endif
 
 // Per-pixel blend state (_kernels.py:41-57 accumulators).  T is the
 // transmittance 1 - A; TRAIN keeps the A-state in float64 for the backward
@@ -80,11 +86,31 @@ struct Blend {
             sy = ay;
             sxy = axy;
         }
+#if RASTER_FFMA2
+        const float2 tg = fmul2(make_float2(t, t), make_float2(gax, gay));        // (t gax, t gay)
+        const float2 txty = fsub2(tg, fmul2(make_float2(sx, sy), make_float2(al, al)));
+        const float tx_ = txty.x, ty_ = txty.y;
+#else
         float tx_ = t * gax - sx * al;
         float ty_ = t * gay - sy * al;
+#endif
         float txy = ((t * gaxy - sy * gax) - sxy * al) - sx * gay;
         float ta = t * al;
         float cc[3] = {col.x, col.y, col.z};
+#if RASTER_FFMA2
+        // (bx, by) and (b, bxy) per channel as packed pairs: 6 FFMA2 instead of 12 FFMA
+        const float2 txy2 = make_float2(tx_, ty_), tab2 = make_float2(ta, txy);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float2 c2 = make_float2(cc[c], cc[c]);
+            const float2 p = ffma2(c2, txy2, make_float2(bx[c], by[c]));
+            const float2 q = ffma2(c2, tab2, make_float2(b[c], bxy[c]));
+            bx[c] = p.x;
+            by[c] = p.y;
+            b[c] = q.x;
+            bxy[c] = q.y;
+        }
+#else
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             bx[c] = fmaf(cc[c], tx_, bx[c]);
@@ -92,6 +118,7 @@ struct Blend {
             bxy[c] = fmaf(cc[c], txy, bxy[c]);
             b[c] = fmaf(cc[c], ta, b[c]);
         }
+#endif
         if (TRAIN) {
             double a = al, gx = gax, gy = gay, gxy = gaxy, o = om;
             double nx = fma(axd, o, Td * gx);
@@ -104,8 +131,13 @@ struct Blend {
             Td = Td * o;
             T = (float)Td;
         } else {
+#if RASTER_FFMA2
+            const float2 nxy2 = ffma2(make_float2(ax, ay), make_float2(om, om), tg);
+            const float nx = nxy2.x, ny = nxy2.y;
+#else
             float nx = fmaf(ax, om, t * gax);
             float ny = fmaf(ay, om, t * gay);
+#endif
             float nxy = (fmaf(axy, om, t * gaxy) - ax * gay) - ay * gax;
             ax = nx;
             ay = ny;
