@@ -8,9 +8,12 @@
 // accumulated-alpha state is inverted in float64 starting from the private
 // float64 terminal state the training forward wrote:
 //   T_{k-1} = T_k / om_k,  A_{x,k-1} = (A_{x,k} - T_{k-1} a_x) / om_k, ...
-// Gradients are reduced without atomics: butterfly shuffles within a warp,
-// then a fixed warp order in shared memory, into one partial per (tile,
-// splat) pair; `reduce_pairs_kernel` sums each splat's pairs in tile order.
+// Each 4x2 lane group walks its own candidate list; per candidate the group's
+// nine gradient terms are reduce-scattered over its 8 lanes, the groups' sums
+// added in fixed order per warp and the warps' in fixed order per batch (a
+// shared-memory ring, the last warp of a batch reducing it), into one partial
+// per (tile, splat) pair; `reduce_pairs_kernel` sums each splat's pairs in
+// tile order.  No atomics: results are bitwise repeatable.
 #include <cmath>
 
 #include "footprint.cuh"
@@ -38,46 +41,6 @@ struct BwdArgs {
     const float* adj;          // (H,W,4,3) w, wx, wy, wxy
     float* partial;            // (pairs, 9) per (splat, tile) partial, emission order
 };
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    return v;
-}
-
-// Warp reduce-scatter of the nine per-lane gradient terms in 14 shuffles (instead of
-// 9 x 5 butterflies): g[0..7] are halved across lane bits 4, 3, 2 (each lane keeps
-// the half its bit selects and adds the partner's copy of it), then summed across
-// bits 1, 0; g[8] is a plain butterfly.  Returns the sum of term
-// term_of_lane(lane) = 4 b4 + 2 b3 + b2 in every lane; `g8` gets the sum of g[8].
-// The summation order is fixed, so results are deterministic.
-__device__ __forceinline__ float warp_reduce9(const float (&g)[kG], int lane, float& g8) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-    float h[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float send = b4 ? g[i] : g[i + 4];
-        const float keep = b4 ? g[i + 4] : g[i];
-        h[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-    float q[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const float send = b3 ? h[i] : h[i + 2];
-        const float keep = b3 ? h[i + 2] : h[i];
-        q[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    float v;
-    {
-        const float send = b2 ? q[0] : q[1];
-        const float keep = b2 ? q[1] : q[0];
-        v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    g8 = warp_sum(g[8]);
-    return v;
-}
 
 // Reduce-scatter of the nine terms over the 8 lanes of a 4x2 group (lane bits
 // 2, 1, 0): lane li of the group ends with the group sum of term li; g8 gets the
@@ -109,12 +72,7 @@ __device__ __forceinline__ float group_reduce9(const float (&g)[kG], int li, flo
     return v;
 }
 
-#ifndef BWD_GROUPS
-#define BWD_GROUPS 1
-#endif
-#ifndef RING_G
-#define RING_G 4
-#endif
+
 
 // Batches of kBwBatch candidates are walked back to front by every warp of the
 // tile independently.  Per-batch, per-warp partials go to one of kRing shared
@@ -122,7 +80,7 @@ __device__ __forceinline__ float group_reduce9(const float (&g)[kG], int li, flo
 // writes the (splat, tile) partials, then releases the slot for batch + kRing.
 // Warps thus drift up to kRing batches apart instead of meeting at a block
 // barrier after every batch (their per-batch work differs with coverage).
-constexpr int kRing = BWD_GROUPS ? RING_G : 8;
+constexpr int kRing = 4;
 
 struct BwdShared {
     struct {
@@ -132,10 +90,8 @@ struct BwdShared {
     float4 col[kWarps_bw][kBwBatch];
     uint32_t rank[kWarps_bw][kBwBatch];
     float part[kRing][kWarps_bw][kBwBatch][kG];
-#if BWD_GROUPS
     float gpart[kWarps_bw][4][kBwBatch][kG];   // per 4x2 group partials of the current batch
     uint8_t list[kWarps_bw][4][kBwBatch];      // per group candidate lists (ascending)
-#endif
     uint32_t touch[kRing][kWarps_bw];
     int done[kRing];
     int epoch[kRing];
@@ -153,13 +109,9 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
     const int tile_x = tile % p.ntx, tile_y = tile / p.ntx;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int rx0 = tile_x * kTile + (warp & 1) * 8, ry0 = tile_y * kTile + (warp >> 1) * 4;
-#if BWD_GROUPS
     // four 4x2 lane groups (as in the forward): group q walks its own candidate list
     const int q = lane >> 3, li = lane & 7;
     const int px = rx0 + (q & 1) * 4 + (li & 3), py = ry0 + (q >> 1) * 2 + (li >> 2);
-#else
-    const int px = rx0 + (lane & 7), py = ry0 + (lane >> 3);
-#endif
     const bool inside = px < p.width && py < p.height;
     const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
     const float X0 = (float)rx0 + 0.5f, Y0 = (float)ry0 + 0.5f;
@@ -236,7 +188,6 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                 s_col[warp][lane] = p.sc.color[r];
             }
         }
-#if BWD_GROUPS
         uint32_t gmask = 0;   // bit g: candidate reaches group g's 4x2 rectangle
         if (keep) {
             const PackF& g = s_pack[warp][lane].f;
@@ -291,23 +242,31 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                     const double ayp = (ay - Tp * (double)gay) * inv;
                     const double axyp = (axy - Tp * (double)gaxy + axp * (double)gay + ayp * (double)gax) * inv;
                     const float t = (float)Tp, sx = (float)axp, sy = (float)ayp, sxy = (float)axyp;
-                    float abar = 0.f, abar_x = 0.f, abar_y = 0.f, abar_xy = 0.f;
+                    // blend coefficients of this splat (_kernels.py:253-262); (x, y) pairs packed
+                    const float ta = t * al;
+                    const float2 cxy = fsub2(fmul2(make_float2(t, t), make_float2(gax, gay)),
+                                             fmul2(make_float2(sx, sy), make_float2(al, al)));
+                    const float cxx = ((t * gaxy - sxy * al) - sy * gax) - sx * gay;
+                    float abar = 0.f, abar_xy = 0.f;
+                    float2 abar_2 = make_float2(0.f, 0.f);   // (abar_x, abar_y)
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         const float W0 = w[c], WX = w[3 + c], WY = w[6 + c], WXY = w[9 + c];
                         const float diff = cc[c] - bh[c];
                         const float u0 = t * diff;
-                        const float u1 = -sx * diff - t * bhx[c];
-                        const float u2 = -sy * diff - t * bhy[c];
+                        // (u2, u1) = (-sy, -sx) diff - t (bhy, bhx)
+                        const float2 u21 = fsub2(fmul2(make_float2(-sy, -sx), make_float2(diff, diff)),
+                                                 fmul2(make_float2(t, t), make_float2(bhy[c], bhx[c])));
+                        const float u1 = u21.y, u2 = u21.x;
                         const float u3 = ((-sxy * diff + sx * bhy[c]) + sy * bhx[c]) - t * bhxy[c];
-                        // _kernels.py:253-262
-                        gr[c] = W0 * (t * al) + WX * (t * gax - sx * al) + WY * (t * gay - sy * al) +
-                                WXY * (((t * gaxy - sxy * al) - sy * gax) - sx * gay);
+                        gr[c] = W0 * ta + WX * cxy.x + WY * cxy.y + WXY * cxx;
                         abar += W0 * u0 + WX * u1 + WY * u2 + WXY * u3;
-                        abar_x += WX * u0 + WXY * u2;
-                        abar_y += WY * u0 + WXY * u1;
+                        // abar_x += WX u0 + WXY u2, abar_y += WY u0 + WXY u1
+                        abar_2 = ffma2(make_float2(WX, WY), make_float2(u0, u0),
+                                       ffma2(make_float2(WXY, WXY), u21, abar_2));
                         abar_xy += WXY * u0;
                     }
+                    const float abar_x = abar_2.x, abar_y = abar_2.y;
                     if (st != kClamped) {   // _kernels.py:291-336
                         const float dx = (cx - g.mxh) - g.mxl, dy = (cy - g.myh) - g.myl;
                         const float ca = g.a, cb = g.b, ccn = g.c;
@@ -315,30 +274,29 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                         const float gy = -(2.f * cb * dx + 2.f * ccn * dy);
                         const float hxy = gx * gy - 2.f * cb;
                         gr[3] = abar * al + abar_x * gax + abar_y * gay + abar_xy * gaxy;   // / sigma later
-                        gr[4] = al * (abar * (-gx) + abar_x * (-gx * gx + 2.f * ca) + abar_y * (-gx * gy + 2.f * cb) +
-                                      abar_xy * (-gx * hxy + 2.f * ca * gy + 2.f * cb * gx));
-                        gr[5] = al * (abar * (-gy) + abar_x * (-gy * gx + 2.f * cb) + abar_y * (-gy * gy + 2.f * ccn) +
-                                      abar_xy * (-gy * hxy + 2.f * cb * gy + 2.f * ccn * gx));
-                        const float dxx = dx * dx, dxy2 = 2.f * dx * dy, dyy = dy * dy;
-                        gr[6] = al * (abar * (-dxx) + abar_x * (-dxx * gx - 2.f * dx) + abar_y * (-dxx * gy) +
-                                      abar_xy * (-dxx * hxy - 2.f * dx * gy));
-                        gr[7] = al * (abar * (-dxy2) + abar_x * (-dxy2 * gx - 2.f * dy) +
-                                      abar_y * (-dxy2 * gy - 2.f * dx) +
-                                      abar_xy * (((-dxy2 * hxy - 2.f * dy * gy) - 2.f * gx * dx) - 2.f));
-                        gr[8] = al * (abar * (-dyy) + abar_x * (-dyy * gx) + abar_y * (-dyy * gy - 2.f * dy) +
-                                      abar_xy * (-dyy * hxy - 2.f * dy * gx));
+                        // the reference's per-parameter sums share S = abar + abar_x gx + abar_y gy
+                        // + abar_xy hxy and P = abar_x + abar_xy gy, Q = abar_y + abar_xy gx:
+                        //   d mean = al (-g S + 2 (a P + b Q, b P + c Q)), d conic = al (-D S - ...)
+                        const float S = ((abar + abar_x * gx) + abar_y * gy) + abar_xy * hxy;
+                        const float P = abar_x + abar_xy * gy, Q = abar_y + abar_xy * gx;
+                        gr[4] = al * (-gx * S + 2.f * (ca * P + cb * Q));
+                        gr[5] = al * (-gy * S + 2.f * (cb * P + ccn * Q));
+                        gr[6] = al * (-(dx * dx) * S - 2.f * dx * P);
+                        gr[7] = al * ((-(2.f * dx * dy) * S - 2.f * dy * P) - 2.f * (dx * Q + abar_xy));
+                        gr[8] = al * (-(dy * dy) * S - 2.f * dy * Q);
                     }
                     // advance the behind-colour state through this splat (_kernels.py:337-357)
                     const float omf = (float)om;
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         const float dcb = cc[c] - bh[c];
-                        const float nbx = omf * bhx[c] + gax * dcb;
-                        const float nby = omf * bhy[c] + gay * dcb;
+                        // (nbx, nby) = omf (bhx, bhy) + (gax, gay) dcb
+                        const float2 nb = ffma2(make_float2(omf, omf), make_float2(bhx[c], bhy[c]),
+                                                fmul2(make_float2(gax, gay), make_float2(dcb, dcb)));
                         const float nbxy = ((omf * bhxy[c] + gaxy * dcb) - gay * bhx[c]) - gax * bhy[c];
                         bh[c] = omf * bh[c] + al * cc[c];
-                        bhx[c] = nbx;
-                        bhy[c] = nby;
+                        bhx[c] = nb.x;
+                        bhy[c] = nb.y;
                         bhxy[c] = nbxy;
                     }
                     T = Tp;
@@ -381,112 +339,6 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
 #pragma unroll
             for (int i = 0; i < kG; ++i) S.part[slot][warp][lane][i] = acc[i];
         }
-#else
-        uint32_t bits = __ballot_sync(0xffffffffu, keep);
-        uint32_t touched = 0;
-        // wait until the slot's previous batch has been reduced
-        if (lane == 0)
-            while (*(volatile int*)&S.epoch[slot] != round) __nanosleep(64);
-        __syncwarp();
-        __threadfence_block();
-        float(*s_part)[kG] = S.part[slot][warp];
-        while (bits) {
-            const int k = 31 - __clz(bits);   // back to front
-            bits &= ~(1u << k);
-            const uint32_t jk = lo + k;
-            float gr[kG];
-#pragma unroll
-            for (int i = 0; i < kG; ++i) gr[i] = 0.f;
-            bool contrib = false;
-            if (live && jk < my_last) {
-                const PackF g = s_pack[warp][k].f;
-                float al, gax, gay, gaxy, rel;
-                int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
-                if (st == kUnsure) {
-                    double a64;
-                    st = eval_exact(p.sc, p.vc, p.bboxes, s_rank[warp][k], px, py, &a64);
-                    if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
-                }
-                if (st != kCulled) {
-                    contrib = true;
-                    const float4 col = s_col[warp][k];
-                    const float cc[3] = {col.x, col.y, col.z};
-                    // invert the accumulated-alpha state across this splat (float64)
-                    const double om = st == kClamped ? (double)1.0e-3f : (double)(1.f - al);
-                    // 1/om: float32 reciprocal refined by two float64 Newton steps (|rel err| ~ 1e-16)
-                    double inv = (double)fast_rcp((float)om);
-                    inv = inv * fma(-om, inv, 2.0);
-                    inv = inv * fma(-om, inv, 2.0);
-                    const double Tp = T * inv;
-                    const double axp = (ax - Tp * (double)gax) * inv;
-                    const double ayp = (ay - Tp * (double)gay) * inv;
-                    const double axyp = (axy - Tp * (double)gaxy + axp * (double)gay + ayp * (double)gax) * inv;
-                    const float t = (float)Tp, sx = (float)axp, sy = (float)ayp, sxy = (float)axyp;
-                    float abar = 0.f, abar_x = 0.f, abar_y = 0.f, abar_xy = 0.f;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float W0 = w[c], WX = w[3 + c], WY = w[6 + c], WXY = w[9 + c];
-                        const float diff = cc[c] - bh[c];
-                        const float u0 = t * diff;
-                        const float u1 = -sx * diff - t * bhx[c];
-                        const float u2 = -sy * diff - t * bhy[c];
-                        const float u3 = ((-sxy * diff + sx * bhy[c]) + sy * bhx[c]) - t * bhxy[c];
-                        // _kernels.py:253-262
-                        gr[c] = W0 * (t * al) + WX * (t * gax - sx * al) + WY * (t * gay - sy * al) +
-                                WXY * (((t * gaxy - sxy * al) - sy * gax) - sx * gay);
-                        abar += W0 * u0 + WX * u1 + WY * u2 + WXY * u3;
-                        abar_x += WX * u0 + WXY * u2;
-                        abar_y += WY * u0 + WXY * u1;
-                        abar_xy += WXY * u0;
-                    }
-                    if (st != kClamped) {   // _kernels.py:291-336
-                        const float dx = (cx - g.mxh) - g.mxl, dy = (cy - g.myh) - g.myl;
-                        const float ca = g.a, cb = g.b, ccn = g.c;
-                        const float gx = -(2.f * ca * dx + 2.f * cb * dy);
-                        const float gy = -(2.f * cb * dx + 2.f * ccn * dy);
-                        const float hxy = gx * gy - 2.f * cb;
-                        gr[3] = abar * al + abar_x * gax + abar_y * gay + abar_xy * gaxy;   // / sigma later
-                        gr[4] = al * (abar * (-gx) + abar_x * (-gx * gx + 2.f * ca) + abar_y * (-gx * gy + 2.f * cb) +
-                                      abar_xy * (-gx * hxy + 2.f * ca * gy + 2.f * cb * gx));
-                        gr[5] = al * (abar * (-gy) + abar_x * (-gy * gx + 2.f * cb) + abar_y * (-gy * gy + 2.f * ccn) +
-                                      abar_xy * (-gy * hxy + 2.f * cb * gy + 2.f * ccn * gx));
-                        const float dxx = dx * dx, dxy2 = 2.f * dx * dy, dyy = dy * dy;
-                        gr[6] = al * (abar * (-dxx) + abar_x * (-dxx * gx - 2.f * dx) + abar_y * (-dxx * gy) +
-                                      abar_xy * (-dxx * hxy - 2.f * dx * gy));
-                        gr[7] = al * (abar * (-dxy2) + abar_x * (-dxy2 * gx - 2.f * dy) +
-                                      abar_y * (-dxy2 * gy - 2.f * dx) +
-                                      abar_xy * (((-dxy2 * hxy - 2.f * dy * gy) - 2.f * gx * dx) - 2.f));
-                        gr[8] = al * (abar * (-dyy) + abar_x * (-dyy * gx) + abar_y * (-dyy * gy - 2.f * dy) +
-                                      abar_xy * (-dyy * hxy - 2.f * dy * gx));
-                    }
-                    // advance the behind-colour state through this splat (_kernels.py:337-357)
-                    const float omf = (float)om;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float dcb = cc[c] - bh[c];
-                        const float nbx = omf * bhx[c] + gax * dcb;
-                        const float nby = omf * bhy[c] + gay * dcb;
-                        const float nbxy = ((omf * bhxy[c] + gaxy * dcb) - gay * bhx[c]) - gax * bhy[c];
-                        bh[c] = omf * bh[c] + al * cc[c];
-                        bhx[c] = nbx;
-                        bhy[c] = nby;
-                        bhxy[c] = nbxy;
-                    }
-                    T = Tp;
-                    ax = axp;
-                    ay = ayp;
-                    axy = axyp;
-                }
-            }
-            if (__any_sync(0xffffffffu, contrib)) {
-                float g8;
-                const float v = warp_reduce9(gr, lane, g8);
-                if ((lane & 3) == 0) s_part[k][lane >> 2] = v;   // term 4 b4 + 2 b3 + b2 = lane / 4
-                if (lane == 1) s_part[k][8] = g8;
-                touched |= 1u << k;
-            }
-        }
-#endif
         // publish; the last warp of the batch reduces the slot
         int prev = 0;
         if (lane == 0) {
