@@ -273,11 +273,12 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                         const float gx = -(2.f * ca * dx + 2.f * cb * dy);
                         const float gy = -(2.f * cb * dx + 2.f * ccn * dy);
                         const float hxy = gx * gy - 2.f * cb;
-                        gr[3] = abar * al + abar_x * gax + abar_y * gay + abar_xy * gaxy;   // / sigma later
                         // the reference's per-parameter sums share S = abar + abar_x gx + abar_y gy
                         // + abar_xy hxy and P = abar_x + abar_xy gy, Q = abar_y + abar_xy gx:
-                        //   d mean = al (-g S + 2 (a P + b Q, b P + c Q)), d conic = al (-D S - ...)
+                        //   d sigma = al S / sigma (the / sigma in the chain), d mean = al (-g S
+                        //   + 2 (a P + b Q, b P + c Q)), d conic = al (-D S - ...)
                         const float S = ((abar + abar_x * gx) + abar_y * gy) + abar_xy * hxy;
+                        gr[3] = al * S;
                         const float P = abar_x + abar_xy * gy, Q = abar_y + abar_xy * gx;
                         gr[4] = al * (-gx * S + 2.f * (ca * P + cb * Q));
                         gr[5] = al * (-gy * S + 2.f * (cb * P + ccn * Q));
