@@ -145,8 +145,12 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
         for (int i = 0; i < 12; ++i) w[i] = 0.f;
     }
     // behind-colour state, the background acting as a far splat (_kernels.py:218-229)
-    float bh[3] = {p.vc.bg[0], p.vc.bg[1], p.vc.bg[2]};
-    float bhx[3] = {0.f, 0.f, 0.f}, bhy[3] = {0.f, 0.f, 0.f}, bhxy[3] = {0.f, 0.f, 0.f};
+    // (channels 0, 1 as packed pairs, channel 2 scalar)
+    float2 bh01 = make_float2(p.vc.bg[0], p.vc.bg[1]), bhx01 = make_float2(0.f, 0.f);
+    float2 bhy01 = make_float2(0.f, 0.f), bhxy01 = make_float2(0.f, 0.f);
+    float bh2 = p.vc.bg[2], bhx2 = 0.f, bhy2 = 0.f, bhxy2 = 0.f;
+    const float2 W0p = make_float2(w[0], w[1]), WXp = make_float2(w[3], w[4]);
+    const float2 WYp = make_float2(w[6], w[7]), WXYp = make_float2(w[9], w[10]);
 
     // block-wide highest list end among live pixels
     uint32_t hi = live ? my_last : start;
@@ -230,7 +234,6 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                 if (st != kCulled) {
                     contrib = true;
                     const float4 col = s_col[warp][idx];
-                    const float cc[3] = {col.x, col.y, col.z};
                     // invert the accumulated-alpha state across this splat (float64)
                     const double om = st == kClamped ? (double)1.0e-3f : (double)(1.f - al);
                     // 1/om: float32 reciprocal refined by two float64 Newton steps (|rel err| ~ 1e-16)
@@ -242,31 +245,42 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                     const double ayp = (ay - Tp * (double)gay) * inv;
                     const double axyp = (axy - Tp * (double)gaxy + axp * (double)gay + ayp * (double)gax) * inv;
                     const float t = (float)Tp, sx = (float)axp, sy = (float)ayp, sxy = (float)axyp;
-                    // blend coefficients of this splat (_kernels.py:253-262); (x, y) pairs packed
+                    // blend coefficients of this splat (_kernels.py:253-262)
                     const float ta = t * al;
                     const float2 cxy = fsub2(fmul2(make_float2(t, t), make_float2(gax, gay)),
                                              fmul2(make_float2(sx, sy), make_float2(al, al)));
                     const float cxx = ((t * gaxy - sxy * al) - sy * gax) - sx * gay;
-                    float abar = 0.f, abar_xy = 0.f;
-                    float2 abar_2 = make_float2(0.f, 0.f);   // (abar_x, abar_y)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float W0 = w[c], WX = w[3 + c], WY = w[6 + c], WXY = w[9 + c];
-                        const float diff = cc[c] - bh[c];
-                        const float u0 = t * diff;
-                        // (u2, u1) = (-sy, -sx) diff - t (bhy, bhx)
-                        const float2 u21 = fsub2(fmul2(make_float2(-sy, -sx), make_float2(diff, diff)),
-                                                 fmul2(make_float2(t, t), make_float2(bhy[c], bhx[c])));
-                        const float u1 = u21.y, u2 = u21.x;
-                        const float u3 = ((-sxy * diff + sx * bhy[c]) + sy * bhx[c]) - t * bhxy[c];
-                        gr[c] = W0 * ta + WX * cxy.x + WY * cxy.y + WXY * cxx;
-                        abar += W0 * u0 + WX * u1 + WY * u2 + WXY * u3;
-                        // abar_x += WX u0 + WXY u2, abar_y += WY u0 + WXY u1
-                        abar_2 = ffma2(make_float2(WX, WY), make_float2(u0, u0),
-                                       ffma2(make_float2(WXY, WXY), u21, abar_2));
-                        abar_xy += WXY * u0;
-                    }
-                    const float abar_x = abar_2.x, abar_y = abar_2.y;
+                    // per-channel adjoint terms u0..u3 and their sums: channels 0 and 1 as
+                    // packed pairs, channel 2 scalar
+                    const float2 T2 = make_float2(t, t);
+                    const float2 d01 = fsub2(make_float2(col.x, col.y), bh01);
+                    const float2 u0p = fmul2(T2, d01);
+                    const float2 u1p = fsub2(fmul2(make_float2(-sx, -sx), d01), fmul2(T2, bhx01));
+                    const float2 u2p = fsub2(fmul2(make_float2(-sy, -sy), d01), fmul2(T2, bhy01));
+                    const float2 u3p = fsub2(ffma2(make_float2(sy, sy), bhx01,
+                                                   ffma2(make_float2(sx, sx), bhy01,
+                                                         fmul2(make_float2(-sxy, -sxy), d01))),
+                                             fmul2(T2, bhxy01));
+                    const float2 grp = ffma2(WXYp, make_float2(cxx, cxx),
+                                             ffma2(WYp, make_float2(cxy.y, cxy.y),
+                                                   ffma2(WXp, make_float2(cxy.x, cxy.x),
+                                                         fmul2(W0p, make_float2(ta, ta)))));
+                    const float2 abp = ffma2(WXYp, u3p, ffma2(WYp, u2p, ffma2(WXp, u1p, fmul2(W0p, u0p))));
+                    const float2 abxp = ffma2(WXp, u0p, fmul2(WXYp, u2p));
+                    const float2 abyp = ffma2(WYp, u0p, fmul2(WXYp, u1p));
+                    const float2 abxyp = fmul2(WXYp, u0p);
+                    const float d2 = col.z - bh2;
+                    const float u0 = t * d2;
+                    const float u1 = -sx * d2 - t * bhx2;
+                    const float u2 = -sy * d2 - t * bhy2;
+                    const float u3 = ((-sxy * d2 + sx * bhy2) + sy * bhx2) - t * bhxy2;
+                    gr[0] = grp.x;
+                    gr[1] = grp.y;
+                    gr[2] = w[2] * ta + w[5] * cxy.x + w[8] * cxy.y + w[11] * cxx;
+                    const float abar = (abp.x + abp.y) + (w[2] * u0 + w[5] * u1 + w[8] * u2 + w[11] * u3);
+                    const float abar_x = (abxp.x + abxp.y) + (w[5] * u0 + w[11] * u2);
+                    const float abar_y = (abyp.x + abyp.y) + (w[8] * u0 + w[11] * u1);
+                    const float abar_xy = (abxyp.x + abxyp.y) + w[11] * u0;
                     if (st != kClamped) {   // _kernels.py:291-336
                         const float dx = (cx - g.mxh) - g.mxl, dy = (cy - g.myh) - g.myl;
                         const float ca = g.a, cb = g.b, ccn = g.c;
@@ -288,17 +302,25 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                     }
                     // advance the behind-colour state through this splat (_kernels.py:337-357)
                     const float omf = (float)om;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float dcb = cc[c] - bh[c];
-                        // (nbx, nby) = omf (bhx, bhy) + (gax, gay) dcb
-                        const float2 nb = ffma2(make_float2(omf, omf), make_float2(bhx[c], bhy[c]),
-                                                fmul2(make_float2(gax, gay), make_float2(dcb, dcb)));
-                        const float nbxy = ((omf * bhxy[c] + gaxy * dcb) - gay * bhx[c]) - gax * bhy[c];
-                        bh[c] = omf * bh[c] + al * cc[c];
-                        bhx[c] = nb.x;
-                        bhy[c] = nb.y;
-                        bhxy[c] = nbxy;
+                    {
+                        const float2 O2 = make_float2(omf, omf);
+                        const float2 GX = make_float2(gax, gax), GY = make_float2(gay, gay);
+                        const float2 nbx = ffma2(O2, bhx01, fmul2(GX, d01));
+                        const float2 nby = ffma2(O2, bhy01, fmul2(GY, d01));
+                        const float2 nbxy = fsub2(fsub2(ffma2(O2, bhxy01, fmul2(make_float2(gaxy, gaxy), d01)),
+                                                        fmul2(GY, bhx01)),
+                                                  fmul2(GX, bhy01));
+                        bh01 = ffma2(O2, bh01, fmul2(make_float2(al, al), make_float2(col.x, col.y)));
+                        bhx01 = nbx;
+                        bhy01 = nby;
+                        bhxy01 = nbxy;
+                        const float nbx2 = omf * bhx2 + gax * d2;
+                        const float nby2 = omf * bhy2 + gay * d2;
+                        const float nbxy2 = ((omf * bhxy2 + gaxy * d2) - gay * bhx2) - gax * bhy2;
+                        bh2 = omf * bh2 + al * col.z;
+                        bhx2 = nbx2;
+                        bhy2 = nby2;
+                        bhxy2 = nbxy2;
                     }
                     T = Tp;
                     ax = axp;
