@@ -166,6 +166,18 @@ int splat_render_backward(const void *scene_const, const splat_scene_t *scene /*
                           const splat_gimg_t *fwd /* host struct */, const float *adjoint, void *workspace,
                           size_t ws_bytes, int64_t pair_capacity, void *bwd_workspace, size_t bwd_bytes,
                           float *grads, int accumulate, void *stream);
+/* The same backward, stopping before the parametrisation chain: adds this
+ * view's render-space terms per rank, (n, 9) float32 [d_colour(3), d_sigma-term,
+ * d_mean (x kx, x ky), d_conic (/ kx^2, / kx ky, / ky^2)], into rank_grads
+ * (accumulate != 0) or overwrites them.  Summed over views, one
+ * splat_chain_grads maps them to parameter gradients: the multi-view training
+ * step pays the chain (raster_backward.py:126-152) once, not once per view. */
+int splat_render_backward_rank(const void *scene_const, const splat_scene_t *scene, const splat_view_t *view,
+                               int width, int height, const splat_gimg_t *fwd, const float *adjoint,
+                               void *workspace, size_t ws_bytes, int64_t pair_capacity, void *bwd_workspace,
+                               size_t bwd_bytes, float *rank_grads, int accumulate, void *stream);
+int splat_chain_grads(const void *scene_const, const splat_scene_t *scene, const float *rank_grads, float *grads,
+                      int accumulate, void *stream);
 
 /* ---- training loss and optimizer ----------------------------------------
  * loss (fit.py:94-108) with ssim_with_grad (baselines.py:170-203):

@@ -78,6 +78,9 @@ SIGNATURES = {
     "splat_backward_workspace_bytes": (SZ, [I64, I64]),
     "splat_render_backward": (I32, [P, ctypes.POINTER(SceneT), ctypes.POINTER(ViewT), I32, I32,
                                     ctypes.POINTER(GimgT), P, P, SZ, I64, P, SZ, P, I32, P]),
+    "splat_render_backward_rank": (I32, [P, ctypes.POINTER(SceneT), ctypes.POINTER(ViewT), I32, I32,
+                                         ctypes.POINTER(GimgT), P, P, SZ, I64, P, SZ, P, I32, P]),
+    "splat_chain_grads": (I32, [P, ctypes.POINTER(SceneT), P, P, I32, P]),
     "splat_loss_workspace_bytes": (SZ, [I32, I32]),
     "splat_loss": (I32, [P, P, I32, I32, D, P, P, P, SZ, P]),
     "splat_adam_step": (I32, [P, P, P, P, I64, D, D, D, D, D, D, P]),

@@ -34,7 +34,9 @@ int adam_impl(double* p, const float* g, double* m, double* v, int64_t count, do
               double bc1, double bc2, double eps, cudaStream_t stream);
 int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, const ViewConst& vc,
                            const FrameLayout& L, char* ws, const splat_gimg_t& fwd, const float* adj,
-                           char* bws, float* grads, int accumulate, cudaStream_t stream);
+                           char* bws, float* grads, int accumulate, cudaStream_t stream, float* rank_out);
+int launch_chain(const SceneConst& sc, const splat_scene_t& scene, const float* rank_grads, float* grads,
+                 int accumulate, cudaStream_t stream);
 int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
                          int clamp, const void* plan, cudaStream_t stream);
 size_t upscale_plan_bytes_impl(int out_w, int out_h);
@@ -198,7 +200,30 @@ int splat_render_backward(const void* scene_const, const splat_scene_t* scene, c
         return set_error(SPLAT_ERR_PARAMETER, "backward workspace too small");
     return launch_raster_backward(scene_const_view(scene_const, scene->n), *scene, make_view_const(*view), L,
                                   (char*)workspace, *fwd, adjoint, (char*)bwd_workspace, grads, accumulate,
-                                  (cudaStream_t)stream);
+                                  (cudaStream_t)stream, nullptr);
+}
+
+int splat_render_backward_rank(const void* scene_const, const splat_scene_t* scene, const splat_view_t* view,
+                               int width, int height, const splat_gimg_t* fwd, const float* adjoint,
+                               void* workspace, size_t ws_bytes, int64_t pair_capacity, void* bwd_workspace,
+                               size_t bwd_bytes, float* rank_grads, int accumulate, void* stream) {
+    int rc = check_dims(width, height);
+    if (rc) return rc;
+    if (!fwd || !fwd->state || !fwd->last)
+        return set_error(SPLAT_ERR_PARAMETER, "backward needs a training-mode forward (state + last)");
+    FrameLayout L = frame_layout(scene->n, width, height, pair_capacity);
+    if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    if (bwd_bytes < backward_workspace_bytes_impl(scene->n, pair_capacity))
+        return set_error(SPLAT_ERR_PARAMETER, "backward workspace too small");
+    return launch_raster_backward(scene_const_view(scene_const, scene->n), *scene, make_view_const(*view), L,
+                                  (char*)workspace, *fwd, adjoint, (char*)bwd_workspace, nullptr, accumulate,
+                                  (cudaStream_t)stream, rank_grads);
+}
+
+int splat_chain_grads(const void* scene_const, const splat_scene_t* scene, const float* rank_grads, float* grads,
+                      int accumulate, void* stream) {
+    return launch_chain(scene_const_view(scene_const, scene->n), *scene, rank_grads, grads, accumulate,
+                        (cudaStream_t)stream);
 }
 
 size_t splat_loss_workspace_bytes(int width, int height) { return loss_workspace_bytes_impl(width, height); }

@@ -405,9 +405,17 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
 // tile-order reduction (raster_backward.py:116-124).  The rank's pairs are the
 // emission slots offsets[r] .. + touched[r] (tile-rectangle order); slot_pos
 // maps each to its list position, where the backward left the partial.
+// Per-term view scales for the rank-order accumulation across views (all 1 for the
+// single-view path): d_mean x kx / ky and d_conic / (kx^2, kx ky, ky^2), so that a
+// view-independent chain (kx = ky = 1) maps the sum over views in one pass.
+struct TermScales {
+    double s[kG];
+};
+
 __global__ void reduce_pairs_kernel(int64_t n, const uint32_t* __restrict__ touched,
                                     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ slot_pos,
-                                    const float* __restrict__ partial, int64_t cap, float* __restrict__ g_rank) {
+                                    const float* __restrict__ partial, int64_t cap, float* __restrict__ g_rank,
+                                    TermScales sc, int accumulate) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     float g[kG];
@@ -421,7 +429,11 @@ __global__ void reduce_pairs_kernel(int64_t n, const uint32_t* __restrict__ touc
         for (int i = 0; i < kG; ++i) g[i] += src[i];
     }
 #pragma unroll
-    for (int i = 0; i < kG; ++i) g_rank[(size_t)r * kG + i] = g[i];
+    for (int i = 0; i < kG; ++i) {
+        const float v = sc.s[i] == 1.0 ? g[i] : (float)((double)g[i] * sc.s[i]);
+        float* d = g_rank + (size_t)r * kG + i;
+        *d = accumulate ? *d + v : v;
+    }
 }
 
 // Per splat, in storage order (coalesced gradient stores): chain the render-space
@@ -468,7 +480,7 @@ size_t backward_workspace_bytes_impl(int64_t n, int64_t cap) {
 
 int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, const ViewConst& vc,
                            const FrameLayout& L, char* ws, const splat_gimg_t& fwd, const float* adj,
-                           char* bws, float* grads, int accumulate, cudaStream_t stream) {
+                           char* bws, float* grads, int accumulate, cudaStream_t stream, float* rank_out) {
     const size_t nn = (size_t)(L.n > 0 ? L.n : 1), cc = (size_t)(L.cap > 0 ? L.cap : 1);
     float* partial = (float*)bws;
     if (L.n == 0) return SPLAT_OK;
@@ -498,12 +510,39 @@ int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, con
     }
     raster_bwd_kernel<<<L.ntx * L.nty, kBlock, sizeof(BwdShared), stream>>>(a); note_launch();
     const int blocks = (int)((L.n + 255) / 256);
+    TermScales ts;
+    for (int i = 0; i < kG; ++i) ts.s[i] = 1.0;
+    if (rank_out) {   // rank-order, view-scaled terms accumulated for one chain over all views
+        ts.s[4] = vc.kx;
+        ts.s[5] = vc.ky;
+        ts.s[6] = 1.0 / (vc.kx * vc.kx);
+        ts.s[7] = 1.0 / (vc.kx * vc.ky);
+        ts.s[8] = 1.0 / (vc.ky * vc.ky);
+        reduce_pairs_kernel<<<blocks, 256, 0, stream>>>(L.n, (const uint32_t*)(ws + L.touched),
+                                                        (const uint32_t*)(ws + L.offsets),
+                                                        (const uint32_t*)(ws + L.slot_pos), partial, L.cap, rank_out,
+                                                        ts, accumulate);
+        note_launch();
+        SPLAT_CUDA_CHECK(cudaGetLastError());
+        return SPLAT_OK;
+    }
     reduce_pairs_kernel<<<blocks, 256, 0, stream>>>(L.n, (const uint32_t*)(ws + L.touched),
                                                     (const uint32_t*)(ws + L.offsets),
-                                                    (const uint32_t*)(ws + L.slot_pos), partial, L.cap, g_rank);
+                                                    (const uint32_t*)(ws + L.slot_pos), partial, L.cap, g_rank, ts, 0);
     note_launch();
     chain_kernel<<<blocks, 256, 0, stream>>>(L.n, sc.rank_of, g_rank, scene.log_scales, scene.rotations, sc.sigma,
                                              vc.kx, vc.ky, accumulate, grads);
+    note_launch();
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
+
+int launch_chain(const SceneConst& sc, const splat_scene_t& scene, const float* rank_grads, float* grads,
+                 int accumulate, cudaStream_t stream) {
+    if (scene.n == 0) return SPLAT_OK;
+    chain_kernel<<<(int)((scene.n + 255) / 256), 256, 0, stream>>>(scene.n, sc.rank_of, rank_grads, scene.log_scales,
+                                                                  scene.rotations, sc.sigma, 1.0, 1.0, accumulate,
+                                                                  grads);
     note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;

@@ -26,7 +26,7 @@ from . import _lib
 from .core import DimensionError, ParameterError, Scene, logit
 from .device import DeviceScene, to_device
 from .distributed import allreduce_grads
-from .raster_backward import GradBuffer, PixelAdjoint, render_backward
+from .raster_backward import GradBuffer, PixelAdjoint, chain_grads, render_backward, render_backward_rank
 from .raster_forward import render_forward
 from .spline import fd_gradients, fd_gradients_backward, upscale_backward, upscale_spline
 
@@ -161,7 +161,9 @@ class ViewTrainer:
         self.values = torch.zeros((max(len(self.views), 1), 2), dtype=torch.float64, device=self.ds.device)
         self.streams = max(1, min(int(self.streams), max(len(self.views), 1)))
         self._streams = [torch.cuda.Stream(device=self.ds.device) for _ in range(self.streams)]
-        self._slot_grads = [self.grads] + [GradBuffer(self.ds.n, self.ds.device) for _ in range(self.streams - 1)]
+        # per stream: render-space gradient terms in rank order, summed over that stream's views
+        self._slot_rank = [torch.empty((max(self.ds.n, 1), 9), dtype=torch.float32, device=self.ds.device)
+                           for _ in range(self.streams)]
         self._adjs = [torch.empty((h, w, 3), dtype=torch.float32, device=self.ds.device)
                       for _ in range(self.streams)]
         self._calibrate()
@@ -227,9 +229,6 @@ class ViewTrainer:
         for st in self._streams:
             st.wait_stream(main)
         self._frames = []
-        for k, st in enumerate(self._streams):
-            with torch.cuda.stream(st):
-                self._slot_grads[k].zero_()
         for i, (v, tgt) in enumerate(zip(self.views, self.targets)):
             k = i % self.streams
             with torch.cuda.stream(self._streams[k]):
@@ -246,14 +245,16 @@ class ViewTrainer:
                 else:
                     adj = PixelAdjoint.zeros(rw, rh, ds.device)
                     adj.planes[:, :, 0, :] = fd_gradients_backward(sadj)
-                render_backward(ds, fwd, adj, out=self._slot_grads[k], accumulate=True, check_finite=False)
+                render_backward_rank(ds, fwd, adj, self._slot_rank[k], accumulate=i >= self.streams)
         for st in self._streams:
             main.wait_stream(st)
         lib = _lib.load()
-        for k in range(1, self.streams):
-            _lib.check(lib.splat_grad_accumulate(_lib.ptr(self.grads.flat), _lib.ptr(self._slot_grads[k].flat),
-                                                 self.grads.flat.numel(), _lib.stream_ptr(main)))
-        allreduce_grads(self.grads.flat, self.group)
+        acc = self._slot_rank[0]
+        for k in range(1, self.streams):   # fixed stream order: deterministic for a fixed `streams`
+            _lib.check(lib.splat_grad_accumulate(_lib.ptr(acc), _lib.ptr(self._slot_rank[k]), acc.numel(),
+                                                 _lib.stream_ptr(main)))
+        allreduce_grads(acc, self.group)   # rank order is the same on every replica
+        chain_grads(ds, acc, self.grads)   # the parametrisation chain once per step (it is linear)
         adam_step(scene_params(ds), grads_dict(self.grads), self.state, self.lrs)
         ds.refresh()   # view-independent terms for the updated parameters (depth order is fixed)
         return self.values

@@ -159,3 +159,35 @@ def render_backward(scene, fwd: GradientImage, adj, *, threads: int = 1, view=No
                                          _lib.stream_ptr()))
     out._ws = bws
     return out.grads()
+
+
+def render_backward_rank(ds: DeviceScene, fwd: GradientImage, adj, rank_grads: torch.Tensor,
+                         accumulate: bool = True) -> torch.Tensor:
+    """Multi-view training building block: add this view's render-space gradient
+    terms, view-scaled and in rank order ((n, 9) float32), into ``rank_grads``;
+    :func:`chain_grads` maps the sum over views to parameter gradients once
+    (raster_backward.py:126-152 applied to the summed terms; the chain is linear)."""
+    h, w = fwd.height, fwd.width
+    pa = _as_adjoint(adj, h, w)
+    if ds.n == 0:
+        return rank_grads
+    if fwd.state is None or fwd.frame is None or fwd.scene is not ds:
+        raise ParameterError("render_backward_rank needs the training-mode forward of this scene")
+    lib = _lib.load()
+    frame = fwd.frame
+    nbytes = lib.splat_backward_workspace_bytes(ds.n, frame.capacity)
+    bws = torch.empty(nbytes, dtype=torch.uint8, device=ds.device)
+    _lib.check(lib.splat_render_backward_rank(_lib.ptr(ds.const), ds.c_scene(), fwd.view, w, h, fwd.c_gimg(),
+                                              _lib.ptr(pa.planes), _lib.ptr(frame.ws), frame.nbytes,
+                                              frame.capacity, _lib.ptr(bws), nbytes, _lib.ptr(rank_grads),
+                                              int(bool(accumulate)), _lib.stream_ptr()))
+    rank_grads._bws = bws   # keep the workspace alive while the stream uses it
+    return rank_grads
+
+
+def chain_grads(ds: DeviceScene, rank_grads: torch.Tensor, out: GradBuffer, accumulate: bool = False) -> GradBuffer:
+    """Parameter gradients (storage order) from summed rank-order terms."""
+    lib = _lib.load()
+    _lib.check(lib.splat_chain_grads(_lib.ptr(ds.const), ds.c_scene(), _lib.ptr(rank_grads), _lib.ptr(out.flat),
+                                     int(bool(accumulate)), _lib.stream_ptr()))
+    return out

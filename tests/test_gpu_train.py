@@ -69,9 +69,11 @@ def test_training_step_matches_reference(P):
         v = 0.001 * gd[k] * gd[k]
         expect = before[k] - lrs[k] * (m / 0.1) / (np.sqrt(v / 0.001) + 1e-8)
         assert np.abs(after[k] - expect).max() < 1e-10, k
-    # and its gradients equal the unfused pieces' (same kernels, same order)
+    # and its gradients equal the unfused pieces' up to the float32 rounding of the
+    # view-scaled rank-order terms (the trainer chains the summed terms once per step)
     for f in FIELDS:
-        assert np.array_equal(tr.grads.grads().numpy()[f], grads[f]), f
+        got, ref = tr.grads.grads().numpy()[f], grads[f]
+        assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max(), f
 
 
 def test_training_reduces_loss(P):
