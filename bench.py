@@ -225,7 +225,7 @@ def train_config(c, world, vpr):
                         "L1+SSIM (lambda 0.2) loss, backward through upscaler and rasterizer; "
                         "grads all-reduced over ranks, then Adam",
             "n_splats": c.n, "render": [c.width, c.height], "output": list(c.out_size),
-            "views_per_rank": vpr, "parallelism": f"view-DP x{world} + NCCL all_reduce(SUM) of 11N fp32 grads"}
+            "views_per_rank": vpr, "parallelism": f"view-DP x{world} + NCCL all_reduce(SUM) of the 9N fp32 rank-order gradient terms"}
 
 
 def cpu_reference_train_view(model, target_img, view, c):

@@ -6,12 +6,13 @@ its analytic adjoint), ``AdamState`` / ``adam_step`` (fit.py:132-160) and
 step of the loop body (fit.py:188-223) over a batch of camera views:
 
     render_forward(train) -> upscale_spline(out_size) -> loss
-    -> upscale_backward -> render_backward (accumulated over views)
-    -> all_reduce(SUM) of the flat gradient buffer over the process group
-    -> adam_step on the float64 parameters
+    -> upscale_backward -> rasterizer backward to rank-order render-space
+       terms (accumulated over views, two views in flight)
+    -> all_reduce(SUM) of the terms over the process group
+    -> parametrisation chain (once) -> adam_step on the float64 parameters
 
 Each rank renders its own views; the only collective is the NCCL all-reduce of
-the 11 N float32 gradients.  All arithmetic runs in
+the 9 N float32 terms.  All arithmetic runs in
 libsplat_b200.so; torch provides the buffers, streams and the collective.
 """
 
