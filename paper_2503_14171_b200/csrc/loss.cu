@@ -238,13 +238,16 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
 }
 
 // value = (1 - lam) * sum|d| / size + lam * (1 - mean_c(sum_ssim_c / inner))
-__global__ void loss_finish_kernel(const double* __restrict__ part_ssim, const float* __restrict__ part_l1,
-                                   int nparts_per_ch, double size, double inner, double lam,
-                                   double* __restrict__ value) {
-    __shared__ double s[3][32];
-    const int lane = threadIdx.x & 31, ch = threadIdx.x >> 5;  // 3 warps
+// 3 x 256 threads: channel c = threadIdx.x / 256 sums its partials with stride 256,
+// then fixed-order warp and block reductions (deterministic).
+__global__ void __launch_bounds__(768) loss_finish_kernel(const double* __restrict__ part_ssim,
+                                                          const float* __restrict__ part_l1, int nparts_per_ch,
+                                                          double size, double inner, double lam,
+                                                          double* __restrict__ value) {
+    __shared__ double s[3][8][2];
+    const int ch = threadIdx.x >> 8, i0 = threadIdx.x & 255, lane = threadIdx.x & 31, wid = i0 >> 5;
     double ss = 0.0, l1 = 0.0;
-    for (int i = lane; i < nparts_per_ch; i += 32) {
+    for (int i = i0; i < nparts_per_ch; i += 256) {
         ss += part_ssim[(size_t)ch * nparts_per_ch + i];
         l1 += (double)part_l1[(size_t)ch * nparts_per_ch + i];
     }
@@ -254,15 +257,20 @@ __global__ void loss_finish_kernel(const double* __restrict__ part_ssim, const f
         l1 += __shfl_xor_sync(0xffffffffu, l1, d);
     }
     if (lane == 0) {
-        s[ch][0] = ss;
-        s[ch][1] = l1;
+        s[ch][wid][0] = ss;
+        s[ch][wid][1] = l1;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double ssim = 0.0, l1t = 0.0;
         for (int c = 0; c < 3; ++c) {
-            ssim += s[c][0] / inner;
-            l1t += s[c][1];
+            double sc = 0.0, lc = 0.0;
+            for (int w = 0; w < 8; ++w) {
+                sc += s[c][w][0];
+                lc += s[c][w][1];
+            }
+            ssim += sc / inner;
+            l1t += lc;
         }
         ssim /= 3.0;
         value[0] = (1.0 - lam) * (l1t / size) + (lam > 0.0 ? lam * (1.0 - ssim) : 0.0);
@@ -352,7 +360,8 @@ int loss_impl(const float* pred, const float* target, int w, int h, double lam, 
     }
     ssim_grad_kernel<<<grid, 256, 0, stream>>>(pred, target, w, h, coef, (float)((1.0 - lam) / size), (float)lam,
                                                adj, part_l1); note_launch();
-    loss_finish_kernel<<<1, 96, 0, stream>>>(part_ssim, part_l1, (int)nparts, size, inner, lam, value); note_launch();
+    loss_finish_kernel<<<1, 768, 0, stream>>>(part_ssim, part_l1, (int)nparts, size, inner, lam, value);
+    note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
