@@ -194,37 +194,68 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
         s_c[2][r][c] = d;
     }
     __syncthreads();
-    for (int e = tid; e < kHalo * kS; e += 256) {
-        const int r = e / kS, c = e - r * kS;
-        float m[3] = {0.f, 0.f, 0.f};
+    // horizontal pass, register-blocked: (row, 4 consecutive columns) per item
+    for (int e = tid; e < kHalo * (kS / 4); e += 256) {
+        const int r = e / (kS / 4), c0 = (e - r * (kS / 4)) * 4;
+        float m[4][3];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const float wk = c_win[k];
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int q = 0; q < 3; ++q) m[q] = fmaf(wk, s_c[q][r][c + k], m[q]);
+            for (int q = 0; q < 3; ++q) m[i][q] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 14; ++t) {
+            float v[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) v[q] = s_c[q][r][c0 + t];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int k = t - i;
+                if (k < 0 || k > 10) continue;
+                const float wk = c_win[k];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) m[i][q] = fmaf(wk, v[q], m[i][q]);
+            }
         }
 #pragma unroll
-        for (int q = 0; q < 3; ++q) s_h[q][r][c] = m[q];
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) s_h[q][r][c0 + i] = m[i][q];
     }
     __syncthreads();
-    for (int e = tid; e < kS * kS; e += 256) {
-        const int r = e / kS, c = e - r * kS;
-        const int gy = Y0 + r, gx = X0 + c;
-        if (gy >= h || gx >= w) continue;
-        float m[3] = {0.f, 0.f, 0.f};
+    // vertical pass, register-blocked: (column, 4 consecutive rows) per thread
+    {
+        const int c = tid & (kS - 1), r0 = (tid >> 5) * 4;
+        float m[4][3];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const float wk = c_win[k];
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int q = 0; q < 3; ++q) m[q] = fmaf(wk, s_h[q][r + k][c], m[q]);
+            for (int q = 0; q < 3; ++q) m[i][q] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 14; ++t) {
+            float v[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) v[q] = s_h[q][r0 + t][c];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int k = t - i;
+                if (k < 0 || k > 10) continue;
+                const float wk = c_win[k];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) m[i][q] = fmaf(wk, v[q], m[i][q]);
+            }
         }
-        const size_t o = ((size_t)gy * w + gx) * 3 + ch;
-        const float x = pred[o], y = target[o];
-        const float dssim = m[0] + 2.f * x * m[1] + y * m[2];
-        const float diff = x - y;
-        const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
-        adj[o] = l1_scale * sgn - lam * dssim;
-        local += fabsf(diff);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int gy = Y0 + r0 + i, gx = X0 + c;
+            if (gy >= h || gx >= w) continue;
+            const size_t o = ((size_t)gy * w + gx) * 3 + ch;
+            const float x = pred[o], y = target[o];
+            const float dssim = m[i][0] + 2.f * x * m[i][1] + y * m[i][2];
+            const float diff = x - y;
+            const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
+            adj[o] = l1_scale * sgn - lam * dssim;
+            local += fabsf(diff);
+        }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
