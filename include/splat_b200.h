@@ -152,6 +152,16 @@ int splat_rasterize(const void *scene_const, int64_t n, const splat_view_t *view
 int splat_view_pack64(const void *scene_const, int64_t n, const splat_view_t *view, double *pack64,
                       void *stream);
 
+/* render_at_points (raster_forward.py:190-233): blended colour (npts,3) float64
+ * at arbitrary positions (render pixels), every valid splat in rank order with
+ * the cull / clamp / early-termination rules; pack64 / valid from a prepared
+ * view (splat_view_pack64, the frame's touched flags), colours (n,3) float64 in
+ * rank order, background (3) host array.  state (npts, 2n) uint8 (may be NULL):
+ * per point the splats that blended, then the ones clamped. */
+int splat_render_points(const double *pack64, const double *colors, const uint8_t *valid, int64_t n,
+                        const double *xs, const double *ys, int64_t npts, const double *background, double *out,
+                        uint8_t *state, void *stream);
+
 /* ---- reverse mode -------------------------------------------------------
  * render_backward (raster_backward.py:73-153) for a frame rendered with
  * train != 0 (its workspace still holds the bins): replays each pixel's

@@ -51,6 +51,9 @@ int gimg_unpack_impl(const float* in, int w, int h, float* planes, float* alpha,
                      cudaStream_t stream);
 int encode_display_impl(const float* img, int64_t n, uint8_t* out, cudaStream_t stream);
 int accumulate_impl(float* dst, const float* src, int64_t n, cudaStream_t stream);
+int points_impl(const double* pack, const double* colors, const uint8_t* valid, int64_t n, const double* xs,
+                const double* ys, int64_t npts, const double* bg, double* out, uint8_t* state,
+                cudaStream_t stream);
 int project_impl(int64_t n, const double* mu, const double* ls3, const double* quat, const double* logit,
                  const splat_camera_t& cam, double* means2, double* ls2, double* rot2, double* logit_out,
                  double* depth, cudaStream_t stream);
@@ -295,6 +298,13 @@ int splat_project_3d(int64_t n, const double* means3, const double* log_scales3,
         return set_error(SPLAT_ERR_PARAMETER, "camera focal lengths and near plane must be positive");
     return project_impl(n, means3, log_scales3, quats, opacity_logits, *camera, means2, log_scales2, rotations,
                         opacity_logits_out, depths, (cudaStream_t)stream);
+}
+
+int splat_render_points(const double* pack64, const double* colors, const uint8_t* valid, int64_t n,
+                        const double* xs, const double* ys, int64_t npts, const double* background, double* out,
+                        uint8_t* state, void* stream) {
+    if (n < 0 || npts < 0) return set_error(SPLAT_ERR_DIMENSION, "negative size");
+    return points_impl(pack64, colors, valid, n, xs, ys, npts, background, out, state, (cudaStream_t)stream);
 }
 
 int splat_grad_accumulate(float* dst, const float* src, int64_t count, void* stream) {

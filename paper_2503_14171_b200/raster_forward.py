@@ -9,9 +9,11 @@ reference guarantees they never change the output).  Extra keywords: ``view``
 (a ``scenes.View`` camera) and ``train`` (keep the float64 terminal state the
 backward pass inverts from).
 
-All work runs in libsplat_b200.so (sm_100a): preprocess -> (tile, rank) pair
-emission -> device radix sort -> tile ranges -> tile rasterizer -> exact
-float64 re-render of the few pixels whose termination was too close to call.
+All work runs in libsplat_b200.so (sm_100a): preprocess -> tile binning
+(per-block histograms, column scan, staged stable fill) -> tile rasterizer ->
+exact float64 re-render of the few pixels whose termination was too close to
+call.  ``render_at_points`` (raster_forward.py:190-233) evaluates the blend at
+arbitrary positions in float64 for finite-difference checks.
 """
 
 from __future__ import annotations
@@ -26,7 +28,7 @@ from .core import ALPHA_CLAMP, ALPHA_CULL, EARLY_TERMINATION, TILE, DimensionErr
 from .device import DeviceScene, to_device
 
 __all__ = ["GradientImage", "RenderPack", "TileBins", "Frame", "sort_by_depth", "prepare_scene",
-           "tile_grid", "bin_tiles", "render_forward", "make_view"]
+           "tile_grid", "bin_tiles", "render_forward", "render_at_points", "make_view"]
 
 PLANES = ("color", "d_dx", "d_dy", "d_dxdy")
 BIN_OFFSETS, BIN_KEYS, BIN_ATOMIC = 1, 2, 4   # splat_bin_tiles flags (include/splat_b200.h)
@@ -307,3 +309,32 @@ def render_forward(scene, out_width: int, out_height: int, *, tiled: bool = True
         _capacity_hint[(ds.n, out_width, out_height)] = cap
     img.frame = frame
     return img
+
+
+def render_at_points(scene, xs, ys, out_width: int, out_height: int, *, with_state: bool = False, view=None):
+    """Blended colour at arbitrary continuous positions (raster_forward.py:190-233),
+    float64 on the device, for finite-difference checks of the gradient planes.
+    Returns an (npts, 3) float64 tensor (and the (npts, 2n) bool blend signature)."""
+    import ctypes
+    lib = _lib.load()
+    pack = prepare_scene(scene, out_width, out_height, view=view)
+    dev = pack.means.device
+    x = torch.as_tensor(np.atleast_1d(np.asarray(xs, np.float64)) if not torch.is_tensor(xs) else xs,
+                        dtype=torch.float64).to(dev).contiguous().reshape(-1)
+    y = torch.as_tensor(np.atleast_1d(np.asarray(ys, np.float64)) if not torch.is_tensor(ys) else ys,
+                        dtype=torch.float64).to(dev).contiguous().reshape(-1)
+    if x.numel() != y.numel():
+        raise DimensionError("xs and ys must have the same length")
+    n, npts = int(pack.sigmas.numel()), x.numel()
+    pack64 = torch.cat([pack.means, pack.conics, pack.sigmas[:, None]], 1).contiguous()
+    cols = pack.colors.to(torch.float64).contiguous()
+    valid = pack.valid.to(torch.uint8).contiguous()
+    out = torch.empty((npts, 3), dtype=torch.float64, device=dev)
+    state = torch.zeros((npts, 2 * n), dtype=torch.uint8, device=dev) if with_state else None
+    ds = to_device(scene)
+    bg = (ctypes.c_double * 3)(*ds.background)
+    _lib.check(lib.splat_render_points(_lib.ptr(pack64), _lib.ptr(cols), _lib.ptr(valid), n, _lib.ptr(x),
+                                       _lib.ptr(y), npts, bg, _lib.ptr(out), _lib.ptr(state), _lib.stream_ptr()))
+    if with_state:
+        return out, state.bool()
+    return out

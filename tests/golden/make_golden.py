@@ -294,6 +294,17 @@ def fit_cases():
              opacity_logits=sc.opacity_logits, colors=sc.colors, depths=sc.depths)
 
 
+def points_case():
+    """render_at_points (raster_forward.py:190-233) at random continuous positions,
+    with the blend signature."""
+    sc = _as_ref(sharp_scene(seed=6, n=40, size=48))
+    rng = np.random.default_rng(12)
+    xs = rng.uniform(-2.0, 50.0, 300)
+    ys = rng.uniform(-2.0, 40.0, 300)
+    out, state = rf.render_at_points(sc, xs, ys, 48, 36, with_state=True)
+    save("points", xs=xs, ys=ys, out=out, state=state, out_w=48, out_h=36, **_scene_arrays(sc))
+
+
 if __name__ == "__main__":
     forward_cases()
     upscale_cases()
@@ -303,3 +314,4 @@ if __name__ == "__main__":
     train_case()
     io_case()
     fit_cases()
+    points_case()

@@ -217,3 +217,52 @@ def test_large_canvas_matches_oracle(P, oracle):
     img = P.render_forward(sc, 2560, 2400)
     ref = oracle.render_forward(sc, 2560, 2400)
     assert_forward_matches(img.numpy(), {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)}, "large")
+
+
+def test_render_at_points_matches_reference(P):
+    """render_at_points vs the reference's own output (float64; blend signature exact)."""
+    g = golden("points")
+    sc = scene_of(g)
+    out, state = P.render_at_points(sc, g["xs"], g["ys"], int(g["out_w"]), int(g["out_h"]), with_state=True)
+    assert np.abs(out.cpu().numpy() - g["out"]).max() < 1e-12
+    assert np.array_equal(state.cpu().numpy(), g["state"])
+
+
+def _smooth_scene(seed, n, size):
+    """Blend smooth over the whole canvas: capped opacities (no early termination),
+    footprints whose 1/255 ellipse covers every pixel (no cull), no clamping."""
+    rng = np.random.default_rng(seed)
+    cap = 1.0 - 1e-3 ** (1.0 / n)
+    sig = rng.uniform(0.3 * cap, cap, n)
+    smin = np.sqrt(2.0) * 0.8 * size / np.sqrt(2.0 * np.log(255.0 * sig.min())) * 1.05   # reach every corner
+    from paper_2503_14171_b200 import Scene, logit
+    return Scene(means=rng.uniform(0.2 * size, 0.8 * size, (n, 2)),
+                 log_scales=np.log(rng.uniform(smin, 1.5 * smin, (n, 2))),
+                 rotations=rng.uniform(-np.pi, np.pi, n), opacity_logits=logit(sig),
+                 colors=rng.uniform(0, 1, (n, 3)), depths=rng.uniform(0, 1, n),
+                 background=rng.uniform(0, 1, 3), reference_resolution=(size, size))
+
+
+def test_gradient_planes_match_finite_differences(P):
+    """Acceptance criterion 1 (test_acceptance.py:32-68): the analytic d/dx, d/dy,
+    d2/dxdy planes vs central differences of render_at_points on smooth scenes."""
+    size, h, h2 = 48, 1e-3, 1e-2
+    ys, xs = np.mgrid[0:size, 0:size]
+    cx, cy = (xs + 0.5).ravel(), (ys + 0.5).ravel()
+    worst = [0.0, 0.0, 0.0]
+    for case in range(5):
+        sc = _smooth_scene(1000 + case, 12 + 8 * case, size)
+        img = P.render_forward(sc, size, size).numpy()
+        assert img["contrib_count"].min() == sc.n
+
+        def at(x, y):
+            return P.render_at_points(sc, x, y, size, size).cpu().numpy().reshape(size, size, 3)
+
+        fdx = (at(cx + h, cy) - at(cx - h, cy)) / (2 * h)
+        fdy = (at(cx, cy + h) - at(cx, cy - h)) / (2 * h)
+        fdxy = (at(cx + h2, cy + h2) - at(cx + h2, cy - h2) - at(cx - h2, cy + h2)
+                + at(cx - h2, cy - h2)) / (4 * h2 * h2)
+        worst[0] = max(worst[0], np.abs(fdx - img["d_dx"]).max())
+        worst[1] = max(worst[1], np.abs(fdy - img["d_dy"]).max())
+        worst[2] = max(worst[2], np.abs(fdxy - img["d_dxdy"]).max())
+    assert worst[0] < 1e-4 and worst[1] < 1e-4 and worst[2] < 1e-3, worst
