@@ -266,3 +266,39 @@ def test_gradient_planes_match_finite_differences(P):
         worst[1] = max(worst[1], np.abs(fdy - img["d_dy"]).max())
         worst[2] = max(worst[2], np.abs(fdxy - img["d_dxdy"]).max())
     assert worst[0] < 1e-4 and worst[1] < 1e-4 and worst[2] < 1e-3, worst
+
+
+def test_spline_reproduces_bicubic_polynomials(P):
+    """Acceptance criterion 2 (test_acceptance.py:71-110): planes sampled from a
+    bicubic polynomial are reproduced exactly at interior samples — here to float32
+    rounding (the reference's float64 bound is 1e-10)."""
+    rng = np.random.default_rng(7)
+    w_in, h_in, factor = 11, 9, 4.0
+    u = (np.arange(w_in, dtype=float) / w_in)[None, :, None]
+    v = (np.arange(h_in, dtype=float) / h_in)[:, None, None]
+    worst = 0.0
+    for _ in range(20):
+        a = rng.normal(0, 0.05, (4, 4))
+
+        def poly(uu, vv, du=0, dv=0):
+            out = 0.0
+            for i in range(du, 4):
+                for j in range(dv, 4):
+                    cu = np.prod(range(i - du + 1, i + 1)) * uu ** (i - du)
+                    cv = np.prod(range(j - dv + 1, j + 1)) * vv ** (j - dv)
+                    out = out + a[i, j] * cu * cv
+            return out + 0.0 * uu * vv
+
+        img = P.GradientImage.from_planes(np.broadcast_to(poly(u, v), (h_in, w_in, 3)),
+                                          np.broadcast_to(poly(u, v, du=1) / w_in, (h_in, w_in, 3)),
+                                          np.broadcast_to(poly(u, v, dv=1) / h_in, (h_in, w_in, 3)),
+                                          np.broadcast_to(poly(u, v, du=1, dv=1) / (w_in * h_in), (h_in, w_in, 3)))
+        out = P.upscale_spline(img, factor, clamp=False).double().cpu().numpy()
+        ho, wo = out.shape[:2]
+        sx = (np.arange(wo) + 0.5) / factor - 0.5
+        sy = (np.arange(ho) + 0.5) / factor - 0.5
+        ix = (np.floor(sx) >= 0) & (np.floor(sx) <= w_in - 2)
+        iy = (np.floor(sy) >= 0) & (np.floor(sy) <= h_in - 2)
+        truth = poly((sx / w_in)[None, :, None], (sy / h_in)[:, None, None])
+        worst = max(worst, float(np.abs(out - truth)[np.ix_(iy, ix)].max()))
+    assert worst < 2e-6, worst
