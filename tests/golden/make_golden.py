@@ -305,6 +305,13 @@ def points_case():
     save("points", xs=xs, ys=ys, out=out, state=state, out_w=48, out_h=36, **_scene_arrays(sc))
 
 
+def recon_case():
+    """The reference's self-reconstruction benchmark target (tests/conftest.py:45-65)."""
+    from conftest import reconstruction_target
+    _, target = reconstruction_target()
+    save("recon_target", target=target)
+
+
 if __name__ == "__main__":
     forward_cases()
     upscale_cases()
@@ -315,3 +322,4 @@ if __name__ == "__main__":
     io_case()
     fit_cases()
     points_case()
+    recon_case()
