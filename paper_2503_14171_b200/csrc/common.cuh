@@ -36,7 +36,7 @@ struct __align__(16) PackF {
     float mxh, myh, mxl, myl;     // render-space mean as float hi + lo parts ((x, y) pairs for FADD2)
     float a, c, b, sigma;         // conic (a, c adjacent for FMUL2) and opacity
     float qcull, qclamp, pad0, pad1;  // ln(255 sigma), ln(sigma / 0.999), b/a, b/c
-    float ex, ey, pad2, pad3;     // half extents of the cull ellipse, padded (pre-filter only)
+    float ex, ey, pad2, pad3;     // half extents of the cull ellipse; pad2: 4x2-group Q-norm bound (pre-filters only)
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

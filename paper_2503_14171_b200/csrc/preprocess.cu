@@ -128,7 +128,15 @@ __global__ void preprocess_kernel(SceneConst sc, ViewConst vc, int width, int he
     // margin: every pixel centre that can contribute lies in mean +- (ex, ey)
     p.ex = (float)(rx * (1.0 + 1e-5) + 1e-3);
     p.ey = (float)(ry * (1.0 + 1e-5) + 1e-3);
-    p.pad2 = 0.f;
+    // group pre-filter of the rasterizer (Q-norm triangle inequality): a 4x2 block of pixel
+    // centres with centre G can hold a pixel with Q(p - m) <= q only if
+    // sqrt(Q(G - m)) <= sqrt(q) + max_{|u|<=1.5,|v|<=.5} sqrt(Q(u, v)); pad2 is that bound squared,
+    // widened by 1e-5 relative + 1e-4 (float32 conic and test rounding are far below)
+    {
+        const double rq = sqrt(2.25 * a + 0.25 * c + 1.5 * fabs(b));
+        const double rt = sqrt(q) + rq;
+        p.pad2 = (float)(rt * rt * (1.0 + 1e-5) + 1e-4);
+    }
     p.pad3 = 0.f;
     pack[r] = p;
 }

@@ -55,7 +55,7 @@ struct Blend {
     float b[3], bx[3], by[3], bxy[3];
     float T, ax, ay, axy;          // float32 state (inference)
     double Td, axd, ayd, axyd;     // float64 state (training)
-    float eps;                     // relative error bound of T
+    float err;                     // absolute error bound of T, excluding the per-step product roundings
     int n;
     uint32_t last;
 
@@ -66,7 +66,7 @@ struct Blend {
         ax = ay = axy = 0.f;
         Td = 1.0;
         axd = ayd = axyd = 0.0;
-        eps = 0.f;
+        err = 0.f;
         n = 0;
         last = 0;
     }
@@ -197,16 +197,17 @@ constexpr int kWarps = kRasterThreads / 32;   // warps per CTA of the persistent
 constexpr int kRects = 8;                     // 8x4 rectangles per 16x16 tile
 
 // One candidate at one pixel: certified decision, blend, termination test.
+// `rp` points at the candidate's rank (read only on the rare exact path).
 template <bool TRAIN>
 __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF& g, const float4& col,
-                                                uint32_t r, uint32_t j, int px, int py, float cx,
+                                                const uint32_t* rp, uint32_t j, int px, int py, float cx,
                                                 float cy, Blend<TRAIN>& s, bool& active, bool& flagged) {
     float al, gax, gay, gaxy, rel;
     int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
     if (st == kCulled) return;
     if (st == kUnsure) {
         double a64;
-        st = eval_exact(p.sc, p.vc, p.bboxes, r, px, py, &a64);
+        st = eval_exact(p.sc, p.vc, p.bboxes, *rp, px, py, &a64);
         if (st == kCulled) return;
         canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
     }
@@ -215,18 +216,22 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
         om = 1.0e-3f;
         rel = 0.f;
     }
+    // Absolute error of T: |om - om_exact| <= al rel, so
+    // err_k <= om err_{k-1} + T_{k-1} al rel (+ one rounding of the product per
+    // step, <= 1.2e-7 T_k including the 1e-3f clamp constant, added at decision
+    // time from the step count n).  No division per step.
+    s.err = fmaf(s.err, om, (s.T * al) * rel);
     s.add(al, gax, gay, gaxy, om, col);
     s.last = j + 1;
-    // relative error bound of T: error of om plus one rounding of the product
-    s.eps += fmaf(al * fast_rcp(om), rel, 1.2e-7f);
-    // T = T_exact (1 +- eps) to first order; 1e-4f and the float compare add < 1e-7.
-    // eps stays far below 1e-2 (flagged pixels stop), so T > 1.02e-4 is never a decision.
+    // err stays far below 1e-6 (flagged pixels stop), so T > 1.02e-4 is never a decision.
     const float T = s.T;
     if (T <= 1.02e-4f) {
-        const float m = fmaf(1.0625f, s.eps, 2e-7f);
-        if (T < kTermF * (1.f - m)) {
+        // 1.0625 covers the first-order terms and the float32 rounding of err itself;
+        // 2.1e-11 the rounding of 1e-4f and of the compares.
+        const float m = fmaf(1.0625f, fmaf((float)s.n, 1.2e-7f * 1.02e-4f, s.err), 2.1e-11f);
+        if (T < kTermF - m) {
             active = false;  // certainly terminated (_kernels.py:110-111)
-        } else if (T <= kTermF * (1.f + m)) {
+        } else if (T <= kTermF + m) {
             active = false;  // too close to call in float32: exact re-render
             flagged = true;
         }
@@ -255,6 +260,9 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 #endif
 #ifndef RASTER_GROUP_EXACT
 #define RASTER_GROUP_EXACT 0
+#endif
+#ifndef RASTER_GROUP_DIL
+#define RASTER_GROUP_DIL 1
 #endif
 #ifndef RASTER_MIN_BLOCKS
 #define RASTER_MIN_BLOCKS 5
@@ -363,6 +371,31 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                         const uint32_t r0 = (ly <= Y0 + 1.f && hy >= Y0) ? 1u : 0u;
                         const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
                         gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
+#if RASTER_GROUP_DIL
+                        // and the Q-norm test at each group centre G: Q(G - m) <= pad2 (see
+                        // preprocess_kernel); the float32 error of Q is <= 8 ulp (t1 + |t2| + t3),
+                        // 2 (t1 + t3) >= t1 + |t2| + t3 for a positive-definite form, so
+                        // 2^-18 (t1 + t3) covers it
+                        if (gmask) {
+                            const float2 d0 = fsub2(fsub2(make_float2(X0 + 1.5f, Y0 + 0.5f), make_float2(g.mxh, g.myh)),
+                                                    make_float2(g.mxl, g.myl));
+                            const float2 dxs = make_float2(d0.x, d0.x + 4.f), dys = make_float2(d0.y, d0.y + 2.f);
+                            const float2 t1 = fmul2(fmul2(make_float2(g.a, g.a), dxs), dxs);
+                            const float2 t3 = fmul2(fmul2(make_float2(g.c, g.c), dys), dys);
+                            const float2 bx = fmul2(make_float2(2.f * g.b, 2.f * g.b), dxs);
+                            // groups 0,1 (row dys.x) and 2,3 (row dys.y)
+                            const float2 s01 = fadd2(t1, make_float2(t3.x, t3.x));
+                            const float2 s23 = fadd2(t1, make_float2(t3.y, t3.y));
+                            const float2 q01 = ffma2(bx, make_float2(dys.x, dys.x), s01);
+                            const float2 q23 = ffma2(bx, make_float2(dys.y, dys.y), s23);
+                            const float2 k = make_float2(-3.8146973e-06f, -3.8146973e-06f);
+                            const float2 l01 = ffma2(s01, k, q01), l23 = ffma2(s23, k, q23);
+                            const float tau = g.pad2;
+                            const uint32_t dm = (l01.x <= tau ? 1u : 0u) | (l01.y <= tau ? 2u : 0u) |
+                                                (l23.x <= tau ? 4u : 0u) | (l23.y <= tau ? 8u : 0u);
+                            gmask &= dm;
+                        }
+#endif
 #endif
                     }
                 }
@@ -400,7 +433,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                         const int idx = __ffs(my_mask) - 1;
                         my_mask &= my_mask - 1u;
                         blend_candidate<TRAIN>(p, S_PACK(warp, b, idx), S_COL(warp, b, idx),
-                                               s_rank[warp][b][idx], base + idx, px, py, cx, cy, s, active,
+                                               &s_rank[warp][b][idx], base + idx, px, py, cx, cy, s, active,
                                                flagged);
                     }
                     if ((k & RASTER_TERM_MASK) == RASTER_TERM_MASK && !__any_sync(0xffffffffu, active)) break;
