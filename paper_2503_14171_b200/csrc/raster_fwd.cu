@@ -200,14 +200,15 @@ constexpr int kRects = 8;                     // 8x4 rectangles per 16x16 tile
 // `rp` points at the candidate's rank (read only on the rare exact path).
 template <bool TRAIN>
 __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF& g, const float4& col,
-                                                const uint32_t* rp, uint32_t j, int px, int py, float cx,
-                                                float cy, Blend<TRAIN>& s, bool& active, bool& flagged) {
+                                                const uint32_t* rp, uint32_t j, float cx, float cy,
+                                                Blend<TRAIN>& s, bool& active, bool& flagged) {
     float al, gax, gay, gaxy, rel;
     int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
     if (st == kCulled) return;
     if (st == kUnsure) {
         double a64;
-        st = eval_exact(p.sc, p.vc, p.bboxes, *rp, px, py, &a64);
+        // (int)cx == px: the centres are px + 0.5, exact in float32
+        st = eval_exact(p.sc, p.vc, p.bboxes, *rp, (int)cx, (int)cy, &a64);
         if (st == kCulled) return;
         canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
     }
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                         const int idx = __ffs(my_mask) - 1;
                         my_mask &= my_mask - 1u;
                         blend_candidate<TRAIN>(p, S_PACK(warp, b, idx), S_COL(warp, b, idx),
-                                               &s_rank[warp][b][idx], base + idx, px, py, cx, cy, s, active,
+                                               &s_rank[warp][b][idx], base + idx, cx, cy, s, active,
                                                flagged);
                     }
                     if ((k & RASTER_TERM_MASK) == RASTER_TERM_MASK && !__any_sync(0xffffffffu, active)) break;
@@ -445,10 +446,11 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
             __syncwarp();
         }
         if (inside) {
-            write_pixel<TRAIN>(p, px, py, s);
+            const int ox = (int)cx, oy = (int)cy;   // == px, py (only the float centres stay live)
+            write_pixel<TRAIN>(p, ox, oy, s);
             if (flagged) {
                 uint32_t slot = atomicAdd(&p.counters[2], 1u);
-                p.fixup[slot] = (uint32_t)(py * p.width + px);
+                p.fixup[slot] = (uint32_t)(oy * p.width + ox);
             }
         }
     }
