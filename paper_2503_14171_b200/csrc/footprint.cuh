@@ -164,6 +164,32 @@ __device__ __forceinline__ void canonical_values(const PackF& g, float cx, float
     axy = al * fmaf(gx, gy, -b2);
 }
 
+// Group pre-filter: bit g set unless the cull ellipse certainly misses 4x2
+// group g of the 8x4 pixel-centre rectangle whose first centre is (X0, Y0)
+// (groups: bit 0 at (X0, Y0), bit 1 at x + 4, bit 2 at y + 2, bit 3 at both).
+// Q-norm triangle inequality at each group centre G: some centre p of the group
+// has Q(p - m) <= q only if Q(G - m) <= pad2 (preprocess_kernel).  The float32
+// error of Q(G - m) is <= 8 ulp (t1 + |t2| + t3) <= 16 ulp (t1 + t3) for a
+// positive-definite form, which the 2^-18 (t1 + t3) allowance covers.
+__device__ __forceinline__ uint32_t group_qnorm_mask(const PackF& g, float X0, float Y0) {
+    const float2 d0 = fsub2(fsub2(make_float2(X0 + 1.5f, Y0 + 0.5f), make_float2(g.mxh, g.myh)),
+                            make_float2(g.mxl, g.myl));
+    const float2 dxs = make_float2(d0.x, d0.x + 4.f), dys = make_float2(d0.y, d0.y + 2.f);
+    const float2 t1 = fmul2(fmul2(make_float2(g.a, g.a), dxs), dxs);
+    const float2 t3 = fmul2(fmul2(make_float2(g.c, g.c), dys), dys);
+    const float2 bx = fmul2(make_float2(2.f * g.b, 2.f * g.b), dxs);
+    // groups 0, 1 (row dys.x) and 2, 3 (row dys.y)
+    const float2 s01 = fadd2(t1, make_float2(t3.x, t3.x));
+    const float2 s23 = fadd2(t1, make_float2(t3.y, t3.y));
+    const float2 q01 = ffma2(bx, make_float2(dys.x, dys.x), s01);
+    const float2 q23 = ffma2(bx, make_float2(dys.y, dys.y), s23);
+    const float2 k = make_float2(-3.8146973e-06f, -3.8146973e-06f);
+    const float2 l01 = ffma2(s01, k, q01), l23 = ffma2(s23, k, q23);
+    const float tau = g.pad2;
+    return (l01.x <= tau ? 1u : 0u) | (l01.y <= tau ? 2u : 0u) | (l23.x <= tau ? 4u : 0u) |
+           (l23.y <= tau ? 8u : 0u);
+}
+
 // Conservative "does the cull ellipse {Q <= qcull} reach the pixel-centre
 // rectangle [X0,X1] x [Y0,Y1]" test.  The minimum of the positive-definite
 // form over the rectangle is at the centre (if inside) or on an edge, where it

@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
             const uint32_t r0 = (ly <= Y0 + 1.f && hy >= Y0) ? 1u : 0u;
             const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
             gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
+            if (gmask) gmask &= group_qnorm_mask(g, X0, Y0);
         }
         const uint32_t lt = (1u << lane) - 1u;
         int cnt_my = 0, cnt_max = 0;

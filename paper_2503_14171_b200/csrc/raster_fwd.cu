@@ -373,29 +373,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                         const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
                         gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
 #if RASTER_GROUP_DIL
-                        // and the Q-norm test at each group centre G: Q(G - m) <= pad2 (see
-                        // preprocess_kernel); the float32 error of Q is <= 8 ulp (t1 + |t2| + t3),
-                        // 2 (t1 + t3) >= t1 + |t2| + t3 for a positive-definite form, so
-                        // 2^-18 (t1 + t3) covers it
-                        if (gmask) {
-                            const float2 d0 = fsub2(fsub2(make_float2(X0 + 1.5f, Y0 + 0.5f), make_float2(g.mxh, g.myh)),
-                                                    make_float2(g.mxl, g.myl));
-                            const float2 dxs = make_float2(d0.x, d0.x + 4.f), dys = make_float2(d0.y, d0.y + 2.f);
-                            const float2 t1 = fmul2(fmul2(make_float2(g.a, g.a), dxs), dxs);
-                            const float2 t3 = fmul2(fmul2(make_float2(g.c, g.c), dys), dys);
-                            const float2 bx = fmul2(make_float2(2.f * g.b, 2.f * g.b), dxs);
-                            // groups 0,1 (row dys.x) and 2,3 (row dys.y)
-                            const float2 s01 = fadd2(t1, make_float2(t3.x, t3.x));
-                            const float2 s23 = fadd2(t1, make_float2(t3.y, t3.y));
-                            const float2 q01 = ffma2(bx, make_float2(dys.x, dys.x), s01);
-                            const float2 q23 = ffma2(bx, make_float2(dys.y, dys.y), s23);
-                            const float2 k = make_float2(-3.8146973e-06f, -3.8146973e-06f);
-                            const float2 l01 = ffma2(s01, k, q01), l23 = ffma2(s23, k, q23);
-                            const float tau = g.pad2;
-                            const uint32_t dm = (l01.x <= tau ? 1u : 0u) | (l01.y <= tau ? 2u : 0u) |
-                                                (l23.x <= tau ? 4u : 0u) | (l23.y <= tau ? 8u : 0u);
-                            gmask &= dm;
-                        }
+                        if (gmask) gmask &= group_qnorm_mask(g, X0, Y0);
 #endif
 #endif
                     }
