@@ -196,22 +196,28 @@ constexpr int kRasterThreads = RASTER_THREADS;
 constexpr int kWarps = kRasterThreads / 32;   // warps per CTA of the persistent raster
 constexpr int kRects = 8;                     // 8x4 rectangles per 16x16 tile
 
-// One candidate at one pixel: certified decision, blend, termination test.
-// `rp` points at the candidate's rank (read only on the rare exact path).
+// One candidate at one pixel: the certified decision (kCulled / kContrib /
+// kClamped) and the canonical float32 values.  `rp` points at the candidate's
+// rank (read only on the rare exact path).
 template <bool TRAIN>
-__device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF& g, const float4& col,
-                                                const uint32_t* rp, uint32_t j, float cx, float cy,
-                                                Blend<TRAIN>& s, bool& active, bool& flagged) {
-    float al, gax, gay, gaxy, rel;
+__device__ __forceinline__ int decide_candidate(const RasterArgs& p, const PackF& g, const uint32_t* rp,
+                                                float cx, float cy, float& al, float& gax, float& gay,
+                                                float& gaxy, float& rel) {
     int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
-    if (st == kCulled) return;
     if (st == kUnsure) {
         double a64;
         // (int)cx == px: the centres are px + 0.5, exact in float32
         st = eval_exact(p.sc, p.vc, p.bboxes, *rp, (int)cx, (int)cy, &a64);
-        if (st == kCulled) return;
-        canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
+        if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
     }
+    return st;
+}
+
+// Blend one contributor (st != kCulled) and run the termination test.
+template <bool TRAIN>
+__device__ __forceinline__ void apply_candidate(int st, float al, float gax, float gay, float gaxy, float rel,
+                                                const float4& col, uint32_t j, Blend<TRAIN>& s, bool& active,
+                                                bool& flagged) {
     float om = 1.f - al;
     if (st == kClamped) {
         om = 1.0e-3f;
@@ -237,6 +243,15 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
             flagged = true;
         }
     }
+}
+
+template <bool TRAIN>
+__device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF& g, const float4& col,
+                                                const uint32_t* rp, uint32_t j, float cx, float cy,
+                                                Blend<TRAIN>& s, bool& active, bool& flagged) {
+    float al, gax, gay, gaxy, rel;
+    const int st = decide_candidate<TRAIN>(p, g, rp, cx, cy, al, gax, gay, gaxy, rel);
+    if (st != kCulled) apply_candidate<TRAIN>(st, al, gax, gay, gaxy, rel, col, j, s, active, flagged);
 }
 
 // Each warp streams the tile's candidate list itself (no block barriers).  The
