@@ -589,6 +589,145 @@ __global__ void __launch_bounds__(256, UP_X4_MINB) upscale_x4_kernel(const float
 #endif
 }
 
+// x2 fast path (C2 / C4).  Same design as the x4 kernel: one thread owns one
+// cell row n and one 4-pixel column group g, i.e. output rows 2n+1, 2n+2
+// (phases 0, 1 of the cell row) x pixels 4g .. 4g+3 (phase 1 of cell 2g-1,
+// phases 0, 1 of cell 2g, phase 0 of cell 2g+1).  Per corner column 2g-1 ..
+// 2g+2 it reads the two corner records (rows n, n+1) once and keeps only the
+// y-pass results G (value-in-x, slope-in-x) of both output rows; the x pass
+// then runs in registers.  A CTA = 8 warps = 8 cell rows x 32 groups (16 x 128
+// output pixels); persistent, TMA-staged source double buffer, TMA bulk stores.
+constexpr int kX2Groups = 32;
+constexpr int kX2CellRows = 8;
+constexpr int kX2SpanC = 2 * kX2Groups + 2;   // corner columns 2 g0 - 1 .. 2 g0 + 64
+constexpr int kX2SpanR = kX2CellRows + 1;
+#ifndef UP_X2_MINB
+#define UP_X2_MINB 2
+#endif
+
+template <bool CLAMP>
+__global__ void __launch_bounds__(256, UP_X2_MINB) upscale_x2_kernel(const float* __restrict__ src, int in_w,
+                                                                     int in_h, float* __restrict__ out,
+                                                                     int out_w, int out_h) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    constexpr size_t kStage = (size_t)kX2SpanR * kX2SpanC * 12;
+    float* const s_src0 = reinterpret_cast<float*>(smem);
+    float4* const s_xp = reinterpret_cast<float4*>(s_src0 + 2 * kStage);  // 8 warps x 2 x 96 float4
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ngx = (out_w / 4 + kX2Groups - 1) / kX2Groups;
+    const int ngy = (in_h + 1 + kX2CellRows - 1) / kX2CellRows;   // cell rows -1 .. in_h-1
+    const int ntiles = ngx * ngy;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[0])));
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    auto box = [&](int t, int& x0, int& ncols, int& y0, int& nrows) {
+        const int g0 = (t % ngx) * kX2Groups, n0 = (t / ngx) * kX2CellRows - 1;
+        x0 = max(2 * g0 - 1, 0);
+        ncols = min(2 * g0 + 2 * kX2Groups, in_w - 1) - x0 + 1;
+        y0 = max(n0, 0);
+        nrows = min(n0 + kX2CellRows, in_h - 1) - y0 + 1;
+    };
+    auto issue = [&](int t, int b) {
+        int x0, ncols, y0, nrows;
+        box(t, x0, ncols, y0, nrows);
+        const uint32_t row_bytes = (uint32_t)ncols * 48u;
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar[b])),
+                     "r"(row_bytes * (uint32_t)nrows)
+                     : "memory");
+        float* dst = s_src0 + (size_t)b * kStage;
+        for (int r = 0; r < nrows; ++r)
+            bulk_copy(dst + (size_t)r * kX2SpanC * 12, src + ((size_t)(y0 + r) * in_w + x0) * 12, row_bytes,
+                      &s_bar[b]);
+    };
+
+    int t = blockIdx.x;
+    if (t < ntiles && tid == 0) issue(t, 0);
+    uint32_t phases = 0u;
+    int sb_i = 0;   // this warp's store buffer (alternates per issued row store)
+    for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
+        if (t + (int)gridDim.x < ntiles && tid == 0) issue(t + gridDim.x, b ^ 1);
+        mbar_wait(&s_bar[b], (phases >> b) & 1u);
+        phases ^= 1u << b;
+        int x0, ncols, y0, nrows;
+        box(t, x0, ncols, y0, nrows);
+        const int gw = (t % ngx) * kX2Groups;        // first group of this tile row
+        const int g = gw + lane;
+        const int n = (t / ngx) * kX2CellRows - 1 + warp;
+        const unsigned active = __ballot_sync(0xffffffffu, g < out_w / 4);
+        if (g < out_w / 4 && n < in_h) {
+            const float* sb = s_src0 + (size_t)b * kStage;
+            const int ra = clampi(n, 0, in_h - 1) - y0, rb = clampi(n + 1, 0, in_h - 1) - y0;
+            // y pass per corner column 2g-1 .. 2g+2 (edge-clamped): G[j][cx] for output row 2n+1+j
+            float G[2][4][6];
+#pragma unroll
+            for (int cx = 0; cx < 4; ++cx) {
+                const int col = clampi(2 * g - 1 + cx, 0, in_w - 1) - x0;
+                const float4* pa = reinterpret_cast<const float4*>(sb + ((size_t)ra * kX2SpanC + col) * 12);
+                const float4* pb = reinterpret_cast<const float4*>(sb + ((size_t)rb * kX2SpanC + col) * 12);
+                const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];
+                const float4 b0 = pb[0], b1 = pb[1], b2 = pb[2];
+                const float a[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+                const float bb[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const float h0 = hermite_w(2, j, 0), h1 = hermite_w(2, j, 1);
+                    const float h2 = hermite_w(2, j, 2), h3 = hermite_w(2, j, 3);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        G[j][cx][c] = fmaf(h0, a[c], fmaf(h1, bb[c], fmaf(h2, a[6 + c], h3 * bb[6 + c])));
+                        G[j][cx][3 + c] = fmaf(h0, a[3 + c], fmaf(h1, bb[3 + c], fmaf(h2, a[9 + c], h3 * bb[9 + c])));
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {              // output row 2n + 1 + j
+                const int v = 2 * n + 1 + j;
+                if (v < 0 || v >= out_h) continue;
+                // x pass: pixel i has phase (i + 1) % 2 in cell 2g - 1 + (i + 1) / 2
+                float o[12];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int jx = (i + 1) % 2, ka = (i + 1) / 2;
+                    const float w0 = hermite_w(2, jx, 0), w1 = hermite_w(2, jx, 1);
+                    const float w2 = hermite_w(2, jx, 2), w3 = hermite_w(2, jx, 3);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float part =
+                            fmaf(w1, G[j][ka + 1][c], fmaf(w2, G[j][ka][3 + c], w3 * G[j][ka + 1][3 + c]));
+                        o[3 * i + c] = CLAMP ? fma_sat(w0, G[j][ka][c], part) : fmaf(w0, G[j][ka][c], part);
+                    }
+                }
+                // the warp's 128 pixels (1536 B) leave as one TMA bulk store
+                float4* w4 = s_xp + (warp * 2 + sb_i) * 96;
+                sb_i ^= 1;
+                if (lane == 0)   // the bulk store that last read this buffer has finished reading
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncwarp(active);
+                w4[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
+                w4[3 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
+                w4[3 * lane + 2] = make_float4(o[8], o[9], o[10], o[11]);
+                float4* d4 = reinterpret_cast<float4*>(out + ((size_t)v * out_w + 4 * gw) * 3);
+                const int nvalid = 3 * min(kX2Groups, out_w / 4 - gw);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp(active);
+                if (lane == 0) {
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d4),
+                                 "r"(smem_u32(w4)), "r"((uint32_t)nvalid * 16u)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            }
+        }
+        __syncthreads();   // stage b is refilled by the prefetch of the next iteration
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ---- backward -----------------------------------------------------------------
 
 constexpr int kBwRows = 16;
@@ -946,12 +1085,37 @@ static int upscale_x4_launch(const float* src, int in_w, int in_h, float* out, i
     return SPLAT_OK;
 }
 
+template <bool CLAMP>
+static int upscale_x2_launch(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
+                             cudaStream_t stream) {
+    const size_t smem = 2 * (size_t)kX2SpanR * kX2SpanC * 48 + 8 * 2 * 96 * 16;
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_x2_kernel<CLAMP>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SPLAT_CUDA_CHECK(
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_x2_kernel<CLAMP>, 256, smem));
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int ntiles = ceil_div(out_w / 4, kX2Groups) * ceil_div(in_h + 1, kX2CellRows);
+    const int grid = max(1, min(ntiles, per_sm * sms));
+    upscale_x2_kernel<CLAMP><<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h); note_launch();
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
+
 int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
                          int clamp, const void* plan, cudaStream_t stream) {
     if (out_w <= 0 || out_h <= 0) return SPLAT_OK;
     if (out_w == 4 * in_w && out_h == 4 * in_h)
         return clamp ? upscale_x4_launch<true>(src, in_w, in_h, out, out_w, out_h, stream)
                      : upscale_x4_launch<false>(src, in_w, in_h, out, out_w, out_h, stream);
+    if (out_w == 2 * in_w && out_h == 2 * in_h && (out_w & 3) == 0)
+        return clamp ? upscale_x2_launch<true>(src, in_w, in_h, out, out_w, out_h, stream)
+                     : upscale_x2_launch<false>(src, in_w, in_h, out, out_w, out_h, stream);
     if (out_w == 2 * in_w && out_h == 2 * in_h)
         return clamp ? upscale_int_launch<2, true>(src, in_w, in_h, out, out_w, out_h, stream)
                      : upscale_int_launch<2, false>(src, in_w, in_h, out, out_w, out_h, stream);

@@ -100,6 +100,22 @@ def test_upscale_backward_x4_matches_oracle(P, oracle, w, h):
         assert np.abs(getattr(got, f).cpu().numpy() - r).max() < 1e-5 * max(1.0, np.abs(r).max()), f
 
 
+@pytest.mark.parametrize("w,h", [(2, 1), (1, 3), (4, 3), (7, 5), (64, 33), (66, 17), (130, 70), (960, 540)])
+@pytest.mark.parametrize("factor", [2.0, 4.0])
+def test_upscale_integer_factors_match_oracle(P, oracle, w, h, factor):
+    """The exact-x2 / x4 kernels (even widths) and the generic integer path (odd widths)
+    vs the oracle, clamped and raw, incl. 1-pixel borders and partial tiles."""
+    rng = np.random.default_rng(w * 1000 + h)
+    planes = [rng.uniform(0, 1, (h, w, 3))] + [rng.normal(0, 0.3, (h, w, 3)) for _ in range(3)]
+    img = P.GradientImage.from_planes(*planes)
+    f32 = [np.asarray(x, dtype=np.float32).astype(np.float64) for x in planes]
+    for clamp in (True, False):
+        got = P.upscale_spline(img, factor, clamp=clamp).cpu().numpy()
+        ref = oracle.upscale_spline(*f32, factor, clamp=clamp)
+        assert got.shape == ref.shape
+        assert np.abs(got - ref).max() < 1e-5, (clamp, np.abs(got - ref).max())
+
+
 def test_binning_paths_agree_at_scale(P):
     """Config-2 scale (200k splats, 960x540): both binning paths give identical lists."""
     from paper_2503_14171_b200.raster_forward import BIN_ATOMIC
