@@ -119,8 +119,9 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
     // |qf - Q_exact| <= ~8 ulp * s; conic/mean rounding adds ~4 ulp * s.  2^-19 * s is a 2x margin.
     // (tol = 0 only when s + qcull = 0, where every test below is "unsure")
     float tol = (s + g.qcull) * 1.9073486e-06f;
-    // |al - alpha_ref| / al <= 2^-21 s (Q) + 2^-20 (exp2 approx, log2e product, sigma, product)
-    rel = fmaf(s, 4.7683716e-07f, 9.5367432e-07f);
+    // |al - alpha_ref| / al <= 2^-21 s (Q) + 2^-20 (exp2 approx, log2e product, sigma, product);
+    // + 2^-24 for the extra rounding of t al in the forward's T' = T - t al
+    rel = fmaf(s, 4.7683716e-07f, 1.0132790e-06f);
     if (qf > g.qcull + tol) return kCulled;
     if (qf >= g.qcull - tol) return kUnsure;
     if (qf <= g.qclamp + tol) {

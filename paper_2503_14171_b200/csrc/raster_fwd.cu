@@ -131,18 +131,20 @@ struct Blend {
             Td = Td * o;
             T = (float)Td;
         } else {
+            // the state advances by this contributor's blend terms:
+            //   A_x' = A_x om + t a_x = A_x + tx, likewise y and xy, and T' = T - t al
+            // (T - ta rounds ta once more: <= 2^-24 ta, carried by eval_fast's `rel`)
 #if RASTER_FFMA2
-            const float2 nxy2 = ffma2(make_float2(ax, ay), make_float2(om, om), tg);
-            const float nx = nxy2.x, ny = nxy2.y;
+            const float2 nxy2 = fadd2(make_float2(ax, ay), make_float2(tx_, ty_));
+            ax = nxy2.x;
+            ay = nxy2.y;
 #else
-            float nx = fmaf(ax, om, t * gax);
-            float ny = fmaf(ay, om, t * gay);
+            ax += tx_;
+            ay += ty_;
 #endif
-            float nxy = (fmaf(axy, om, t * gaxy) - ax * gay) - ay * gax;
-            ax = nx;
-            ay = ny;
-            axy = nxy;
-            T = T * om;
+            axy += txy;
+            T -= ta;
+            (void)om;
         }
         ++n;
     }
