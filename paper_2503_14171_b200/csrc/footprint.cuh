@@ -102,6 +102,9 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     return bits_f2(r);
 }
 
+// RAW: return the gradient factors (gx, gy, h = gx gy - 2b) instead of
+// (al gx, al gy, al h) — the inference blend multiplies by al itself.
+template <bool RAW = false>
 __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, float& al, float& ax,
                                          float& ay, float& axy, float& rel) {
     // (dx, dy) = ((cx, cy) - (mxh, myh)) - (mxl, myl), and (a dx, c dy) as packed pairs
@@ -137,14 +140,21 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
     al = g.sigma * fast_exp2(-1.44269504f * qf);
     // (gx, gy) = -2 ((b dy, b dx) + (a dx, c dy))
     const float2 gxy = fmul2(ffma2(make_float2(g.b, g.b), make_float2(dy, dx), acd), make_float2(-2.f, -2.f));
-    const float2 axy2 = fmul2(make_float2(al, al), gxy);
-    ax = axy2.x;
-    ay = axy2.y;
-    axy = al * fmaf(gxy.x, gxy.y, -b2);
+    if (RAW) {
+        ax = gxy.x;
+        ay = gxy.y;
+        axy = fmaf(gxy.x, gxy.y, -b2);
+    } else {
+        const float2 axy2 = fmul2(make_float2(al, al), gxy);
+        ax = axy2.x;
+        ay = axy2.y;
+        axy = al * fmaf(gxy.x, gxy.y, -b2);
+    }
     return kContrib;
 }
 
 // Values of a candidate whose decision came from the exact path.
+template <bool RAW = false>
 __device__ __forceinline__ void canonical_values(const PackF& g, float cx, float cy, int st, float& al,
                                                  float& ax, float& ay, float& axy) {
     if (st == kClamped) {
@@ -160,9 +170,15 @@ __device__ __forceinline__ void canonical_values(const PackF& g, float cx, float
     al = g.sigma * fast_exp2(-1.44269504f * qf);
     float gx = -2.f * fmaf(g.b, dy, adx);
     float gy = -2.f * fmaf(g.b, dx, g.c * dy);
-    ax = al * gx;
-    ay = al * gy;
-    axy = al * fmaf(gx, gy, -b2);
+    if (RAW) {
+        ax = gx;
+        ay = gy;
+        axy = fmaf(gx, gy, -b2);
+    } else {
+        ax = al * gx;
+        ay = al * gy;
+        axy = al * fmaf(gx, gy, -b2);
+    }
 }
 
 // Group pre-filter: bit g set unless the cull ellipse certainly misses 4x2

@@ -71,6 +71,35 @@ struct Blend {
         last = 0;
     }
 
+    // Inference blend from the raw gradient factors (gx, gy, h = gx gy - 2b; zero when
+    // clamped): a_x = al gx etc. are folded into the blend terms
+    //   tx = al (T gx - A_x),  ty = al (T gy - A_y),  txy = al (T h - A_y gx - A_x gy - A_xy)
+    // and the state advances by them (A_x += tx, T -= T al).
+    __device__ __forceinline__ void add_raw(float al, float gx, float gy, float h, const float4& col) {
+        const float2 al2 = make_float2(al, al);
+        const float2 txty = fmul2(al2, ffma2(make_float2(T, T), make_float2(gx, gy), make_float2(-ax, -ay)));
+        const float txy = al * fmaf(-ax, gy, fmaf(-ay, gx, fmaf(T, h, -axy)));
+        const float ta = T * al;
+        const float2 tab2 = make_float2(ta, txy);
+        const float cc[3] = {col.x, col.y, col.z};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float2 c2 = make_float2(cc[c], cc[c]);
+            const float2 p = ffma2(c2, txty, make_float2(bx[c], by[c]));
+            const float2 q = ffma2(c2, tab2, make_float2(b[c], bxy[c]));
+            bx[c] = p.x;
+            by[c] = p.y;
+            b[c] = q.x;
+            bxy[c] = q.y;
+        }
+        const float2 n2 = fadd2(make_float2(ax, ay), txty);
+        ax = n2.x;
+        ay = n2.y;
+        axy += txy;
+        T -= ta;
+        ++n;
+    }
+
     // One contributor (_kernels.py:88-109).  om = 1 - alpha (exactly 1e-3 when clamped).
     __device__ __forceinline__ void add(float al, float gax, float gay, float gaxy, float om,
                                         const float4& col) {
@@ -205,12 +234,13 @@ template <bool TRAIN>
 __device__ __forceinline__ int decide_candidate(const RasterArgs& p, const PackF& g, const uint32_t* rp,
                                                 float cx, float cy, float& al, float& gax, float& gay,
                                                 float& gaxy, float& rel) {
-    int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
+    // inference: raw gradient factors (see Blend::add_raw); training: al-scaled
+    int st = eval_fast<!TRAIN>(g, cx, cy, al, gax, gay, gaxy, rel);
     if (st == kUnsure) {
         double a64;
         // (int)cx == px: the centres are px + 0.5, exact in float32
         st = eval_exact(p.sc, p.vc, p.bboxes, *rp, (int)cx, (int)cy, &a64);
-        if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
+        if (st != kCulled) canonical_values<!TRAIN>(g, cx, cy, st, al, gax, gay, gaxy);
     }
     return st;
 }
@@ -230,7 +260,8 @@ __device__ __forceinline__ void apply_candidate(int st, float al, float gax, flo
     // step, <= 1.2e-7 T_k including the 1e-3f clamp constant, added at decision
     // time from the step count n).  No division per step.
     s.err = fmaf(s.err, om, (s.T * al) * rel);
-    s.add(al, gax, gay, gaxy, om, col);
+    if (TRAIN) s.add(al, gax, gay, gaxy, om, col);
+    else s.add_raw(al, gax, gay, gaxy, col);
     s.last = j + 1;
     // err stays far below 1e-6 (flagged pixels stop), so T > 1.02e-4 is never a decision.
     const float T = s.T;
