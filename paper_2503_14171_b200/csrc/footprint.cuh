@@ -133,6 +133,9 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
             ax = 0.f;
             ay = 0.f;
             axy = 0.f;
+            // 1 - 0.999f = 1e-3 (1 - 1.3e-5): the inference blend's T - T al carries that
+            // relative error of om (= 1.3e-8 / al), which this bound covers
+            rel = 1.6e-5f;
             return kClamped;
         }
         return kUnsure;

@@ -241,6 +241,7 @@ __device__ __forceinline__ int decide_candidate(const RasterArgs& p, const PackF
         // (int)cx == px: the centres are px + 0.5, exact in float32
         st = eval_exact(p.sc, p.vc, p.bboxes, *rp, (int)cx, (int)cy, &a64);
         if (st != kCulled) canonical_values<!TRAIN>(g, cx, cy, st, al, gax, gay, gaxy);
+        if (st == kClamped) rel = 1.6e-5f;   // as eval_fast's clamped branch
     }
     return st;
 }
@@ -250,11 +251,11 @@ template <bool TRAIN>
 __device__ __forceinline__ void apply_candidate(int st, float al, float gax, float gay, float gaxy, float rel,
                                                 const float4& col, uint32_t j, Blend<TRAIN>& s, bool& active,
                                                 bool& flagged) {
+    // training keeps the reference's om = 1e-3 for clamped splats (the backward inverts
+    // with it); inference advances T by T al and uses om = 1 - al only in the error
+    // recurrence, with the clamped `rel` of eval_fast covering 1 - 0.999f != 1e-3
     float om = 1.f - al;
-    if (st == kClamped) {
-        om = 1.0e-3f;
-        rel = 0.f;
-    }
+    if (TRAIN && st == kClamped) om = 1.0e-3f;
     // Absolute error of T: |om - om_exact| <= al rel, so
     // err_k <= om err_{k-1} + T_{k-1} al rel (+ one rounding of the product per
     // step, <= 1.2e-7 T_k including the 1e-3f clamp constant, added at decision
