@@ -260,7 +260,8 @@ __device__ __forceinline__ void apply_candidate(int st, float al, float gax, flo
     // err_k <= om err_{k-1} + T_{k-1} al rel (+ one rounding of the product per
     // step, <= 1.2e-7 T_k including the 1e-3f clamp constant, added at decision
     // time from the step count n).  No division per step.
-    s.err = fmaf(s.err, om, (s.T * al) * rel);
+    if (TRAIN) s.err = fmaf(s.err, om, (s.T * al) * rel);
+    else s.err = fmaf(-s.err, al, fmaf(s.T * al, rel, s.err));   // err (1 - al) + ta rel, no om
     if (TRAIN) s.add(al, gax, gay, gaxy, om, col);
     else s.add_raw(al, gax, gay, gaxy, col);
     s.last = j + 1;
