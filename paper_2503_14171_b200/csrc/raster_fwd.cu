@@ -318,6 +318,9 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 #ifndef RASTER_MIN_BLOCKS
 #define RASTER_MIN_BLOCKS 5
 #endif
+#ifndef RASTER_UNROLL
+#define RASTER_UNROLL 2
+#endif
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
                  "l"(gmem)
@@ -451,6 +454,25 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                 }
 #endif
                 __syncwarp();
+#if RASTER_UNROLL > 1 && !RASTER_STATS
+                // RASTER_UNROLL steps per iteration in inference (a step with an empty list is a
+                // no-op, so the tail needs no guard): less loop-back and termination-vote
+                // overhead.  Training keeps one step (its float64 state has no registers to spare).
+                constexpr int kU = TRAIN ? 1 : RASTER_UNROLL;
+                for (int k = 0; k < cnt_max; k += kU) {
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        if (active && my_mask != 0u) {
+                            const int idx = __ffs(my_mask) - 1;
+                            my_mask &= my_mask - 1u;
+                            blend_candidate<TRAIN>(p, S_PACK(warp, b, idx), S_COL(warp, b, idx),
+                                                   &s_rank[warp][b][idx], base + idx, cx, cy, s, active,
+                                                   flagged);
+                        }
+                    }
+                    if (((k + kU) & 7) == 0 && !__any_sync(0xffffffffu, active)) break;
+                }
+#else
                 for (int k = 0; k < cnt_max; ++k) {
 #if RASTER_STATS
                     {
@@ -467,6 +489,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                     }
                     if ((k & RASTER_TERM_MASK) == RASTER_TERM_MASK && !__any_sync(0xffffffffu, active)) break;
                 }
+#endif
                 if (!__any_sync(0xffffffffu, active)) break;
                 __syncwarp();
             }
