@@ -172,18 +172,24 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
     for (uint32_t e = (hi - start) * kG + tid; e < (end - start) * kG; e += kBlock)
         p.partial[(size_t)start * kG + e] = 0.f;
 
-    for (uint32_t top = hi; top > start;
-         top = (top - start > (uint32_t)kBwBatch) ? top - kBwBatch : start, ++bi) {
-        const uint32_t lo = (top - start > (uint32_t)kBwBatch) ? top - kBwBatch : start;
+    // the batch's ranks are loaded one batch ahead (one dependent global load less per batch)
+    auto batch_lo = [&](uint32_t tp) { return (tp - start > (uint32_t)kBwBatch) ? tp - kBwBatch : start; };
+    uint32_t r_cur = 0;
+    if (hi > start && batch_lo(hi) + lane < hi) r_cur = p.ranks[batch_lo(hi) + lane];
+    for (uint32_t top = hi; top > start; top = batch_lo(top), ++bi) {
+        const uint32_t lo = batch_lo(top);
         const int nb = (int)(top - lo);
         const int slot = bi % kRing, round = bi / kRing;
+        const uint32_t r = r_cur;
+        if (lo > start) {
+            const uint32_t lo2 = batch_lo(lo);
+            r_cur = lo2 + lane < lo ? p.ranks[lo2 + lane] : 0u;
+        }
         // this warp stages the batch and culls it against its own rectangle
         // (skipped when none of its live pixels reaches back this far)
         const bool work = lo < warp_hi;
-        const uint32_t j = lo + lane;
         bool keep = false;
         if (lane < nb) {
-            const uint32_t r = p.ranks[j];
             s_rank[warp][lane] = r;
             if (work) {
                 const PackF g = p.pack[r];
