@@ -428,12 +428,26 @@ __global__ void reduce_pairs_kernel(int64_t n, const uint32_t* __restrict__ touc
     float g[kG];
 #pragma unroll
     for (int i = 0; i < kG; ++i) g[i] = 0.f;
-    const uint32_t off = offsets[r], cnt = touched[r];
-    for (uint32_t k = 0; k < cnt; ++k) {
-        if ((int64_t)(off + k) >= cap) break;
-        const float* src = partial + (size_t)slot_pos[off + k] * kG;
+    const uint32_t off = offsets[r];
+    const uint32_t cnt = (uint32_t)min((int64_t)touched[r], cap - (int64_t)off > 0 ? cap - (int64_t)off : (int64_t)0);
+    // four pairs' gathers in flight at a time, summed in tile order
+    for (uint32_t k = 0; k < cnt; k += 4) {
+        uint32_t pos[4];
 #pragma unroll
-        for (int i = 0; i < kG; ++i) g[i] += src[i];
+        for (int u = 0; u < 4; ++u) pos[u] = k + u < cnt ? slot_pos[off + k + u] : 0xffffffffu;
+        float v[4][kG];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float* src = partial + (size_t)(pos[u] == 0xffffffffu ? 0u : pos[u]) * kG;
+#pragma unroll
+            for (int i = 0; i < kG; ++i) v[u][i] = pos[u] == 0xffffffffu ? 0.f : __ldg(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (pos[u] != 0xffffffffu) {
+#pragma unroll
+                for (int i = 0; i < kG; ++i) g[i] += v[u][i];
+            }
     }
 #pragma unroll
     for (int i = 0; i < kG; ++i) {
