@@ -136,3 +136,49 @@ def test_prefetched_targets_give_the_same_steps(P):
         assert torch.equal(va, vb)
     for k in fit.scene_params(a.ds):
         assert torch.equal(fit.scene_params(a.ds)[k], fit.scene_params(b.ds)[k]), k
+
+
+def test_view_parallel_step_equals_oracle_sum_of_views(P, oracle, monkeypatch):
+    """Config 5's multi-GPU decomposition on one GPU: two "ranks" (trainers over views
+    {0, 1} and {2, 3}) whose rank-order gradient terms are summed where the NCCL
+    all-reduce sits, then chained once — equals the oracle's sum over the four views
+    (1e-3 relative) and the single-rank four-view step (float32 order only)."""
+    import torch
+    from paper_2503_14171_b200 import fit
+    from paper_2503_14171_b200.scenes import random_views, synthetic_scene, view_scene
+    model = synthetic_scene(2000, 96, 64, (2.0, 6.0), seed=5)
+    tsc = synthetic_scene(2000, 96, 64, (2.0, 6.0), seed=7)
+    views = random_views(4, 96, 64, seed=3)
+    tg = [P.render_forward(tsc, 96, 64, view=v).color.clamp(0, 1).contiguous() for v in views]
+    captured = {}
+
+    def rank1_allreduce(flat, group=None):     # rank 1's contribution to the all-reduce
+        captured["b"] = flat.clone()
+        return flat
+
+    def rank0_allreduce(flat, group=None):     # rank 0 receives the SUM
+        flat.add_(captured["b"])
+        return flat
+
+    b = fit.ViewTrainer(model.copy(), (24, 16), (96, 64), views[2:], tg[2:])
+    monkeypatch.setattr(fit, "allreduce_grads", rank1_allreduce)
+    b.step()
+    a = fit.ViewTrainer(model.copy(), (24, 16), (96, 64), views[:2], tg[:2])
+    monkeypatch.setattr(fit, "allreduce_grads", rank0_allreduce)
+    a.step()
+    monkeypatch.undo()
+    full = fit.ViewTrainer(model.copy(), (24, 16), (96, 64), views, tg)
+    full.step()
+    got, one = a.grads.grads().numpy(), full.grads.grads().numpy()
+    ref = None
+    for v, t in zip(views, tg):
+        sv = view_scene(model, v)
+        fwd = oracle.render_forward(sv, 24, 16)
+        pred = oracle.upscale_spline(fwd.color, fwd.d_dx, fwd.d_dy, fwd.d_dxdy, 4.0, out_size=(96, 64))
+        _, dpred = oracle.loss(pred, t.double().cpu().numpy(), 0.2)
+        sadj = oracle.upscale_backward(24, 16, 4.0, dpred, out_size=(96, 64))
+        gv = oracle.render_backward(sv, fwd, sadj)
+        ref = gv if ref is None else {f: ref[f] + gv[f] for f in FIELDS}
+    for f in FIELDS:
+        assert rel_err(got[f], ref[f]) < 1e-3, (f, rel_err(got[f], ref[f]))
+        assert np.abs(got[f] - one[f]).max() <= 1e-5 * np.abs(one[f]).max(), f
