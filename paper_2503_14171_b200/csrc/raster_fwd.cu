@@ -517,8 +517,17 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
 //      float64 accumulation `acc = acc + alpha * (1 - acc)` for the
 //      termination decision (_kernels.py:105-111) and the same float32 (or
 //      TRAIN float64) value recurrences as the main pass.
-constexpr int kFixSeg = 2048;
-constexpr int kFixThreads = 512;
+#ifndef FIX_SEG
+#define FIX_SEG 2048
+#endif
+#ifndef FIX_THREADS
+#define FIX_THREADS 512
+#endif
+#ifndef FIX_GRID
+#define FIX_GRID (148 * 2)
+#endif
+constexpr int kFixSeg = FIX_SEG;
+constexpr int kFixThreads = FIX_THREADS;
 constexpr int kFixPer = kFixSeg / kFixThreads;
 
 struct FixShared {
@@ -676,10 +685,10 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
     SPLAT_CUDA_CHECK(cudaMemsetAsync(a.counters + 2, 0, 8, stream));
     if (train) {
         raster_fwd_kernel<true><<<grid_train, kRasterThreads, 0, stream>>>(a); note_launch();
-        fixup_kernel<true><<<148 * 2, kFixThreads, sizeof(FixShared), stream>>>(a); note_launch();
+        fixup_kernel<true><<<FIX_GRID, kFixThreads, sizeof(FixShared), stream>>>(a); note_launch();
     } else {
         raster_fwd_kernel<false><<<grid_inf, kRasterThreads, 0, stream>>>(a); note_launch();
-        fixup_kernel<false><<<148 * 2, kFixThreads, sizeof(FixShared), stream>>>(a); note_launch();
+        fixup_kernel<false><<<FIX_GRID, kFixThreads, sizeof(FixShared), stream>>>(a); note_launch();
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
