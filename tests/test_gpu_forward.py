@@ -205,6 +205,26 @@ def test_views_match_oracle(P, oracle):
         assert_forward_matches(img.numpy(), {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)})
 
 
+def test_headline_view_matches_oracle_c3_scale(P, oracle):
+    """The headline workload at full size (C3: 1M splats, 960x540, one zoom/pan view of
+    the bench's batch, x4 to 3840x2160): contrib_count bit-exact, planes <= 1e-4, the
+    4K frame <= 1e-4 and PSNR >= 60 dB against the float64 oracle."""
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    from paper_2503_14171_b200.scenes import CONFIGS, random_views, synthetic_scene, view_scene
+    c = CONFIGS["c3"]
+    sc = synthetic_scene(c.n, c.width, c.height, c.scale_range, seed=5)
+    v = random_views(c.views, c.width, c.height, seed=11)[7]   # as bench.py's batch
+    img = P.render_forward(sc, c.width, c.height, view=v)
+    ref = oracle.render_forward(view_scene(sc, v), c.width, c.height)
+    assert_forward_matches(img.numpy(), {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)}, "c3")
+    refup = oracle.upscale_spline(ref.color, ref.d_dx, ref.d_dy, ref.d_dxdy, c.factor)
+    pipe = ViewPipeline(sc, c.width, c.height, factor=c.factor, slots=1)
+    up = pipe.render([v], keep=True)[0].cpu().numpy()
+    diff = up - refup
+    assert np.abs(diff).max() < PLANE_TOL
+    assert 10 * np.log10(1.0 / np.mean(diff ** 2)) >= 60.0
+
+
 def test_forward_is_deterministic(P):
     import torch
     sc = ref_fixture_scene(5, 2000, 128)
