@@ -723,6 +723,9 @@ __global__ void __launch_bounds__(256, UP_X2_MINB) upscale_x2_kernel(const float
                 }
             }
         }
+        // lanes past the image's right edge skip the stores: keep the store-buffer parity
+        // warp-uniform (lane 0 stores whenever the warp stores)
+        sb_i = __shfl_sync(0xffffffffu, sb_i, 0);
         __syncthreads();   // stage b is refilled by the prefetch of the next iteration
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

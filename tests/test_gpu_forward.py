@@ -100,7 +100,8 @@ def test_upscale_backward_x4_matches_oracle(P, oracle, w, h):
         assert np.abs(getattr(got, f).cpu().numpy() - r).max() < 1e-5 * max(1.0, np.abs(r).max()), f
 
 
-@pytest.mark.parametrize("w,h", [(2, 1), (1, 3), (4, 3), (7, 5), (64, 33), (66, 17), (130, 70), (960, 540)])
+@pytest.mark.parametrize("w,h", [(2, 1), (1, 3), (4, 3), (7, 5), (64, 33), (66, 17), (130, 70), (960, 540),
+                                 (1080, 540), (1080, 1200), (1366, 97)])
 @pytest.mark.parametrize("factor", [2.0, 4.0])
 def test_upscale_integer_factors_match_oracle(P, oracle, w, h, factor):
     """The exact-x2 / x4 kernels (even widths) and the generic integer path (odd widths)
@@ -217,6 +218,25 @@ def test_headline_view_matches_oracle_c3_scale(P, oracle):
     img = P.render_forward(sc, c.width, c.height, view=v)
     ref = oracle.render_forward(view_scene(sc, v), c.width, c.height)
     assert_forward_matches(img.numpy(), {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)}, "c3")
+    refup = oracle.upscale_spline(ref.color, ref.d_dx, ref.d_dy, ref.d_dxdy, c.factor)
+    pipe = ViewPipeline(sc, c.width, c.height, factor=c.factor, slots=1)
+    up = pipe.render([v], keep=True)[0].cpu().numpy()
+    diff = up - refup
+    assert np.abs(diff).max() < PLANE_TOL
+    assert 10 * np.log10(1.0 / np.mean(diff ** 2)) >= 60.0
+
+
+def test_stereo_eye_matches_oracle_c4_scale(P, oracle):
+    """C4 at full size: one eye of a stereo pair (3M splats, 1080x1200 render, exact-x2
+    upscale to 2160x2400) against the oracle."""
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    from paper_2503_14171_b200.scenes import CONFIGS, stereo_views, synthetic_scene, view_scene
+    c = CONFIGS["c4"]
+    sc = synthetic_scene(c.n, c.width, c.height, c.scale_range, seed=5)
+    v = stereo_views(1, c.width, c.height, seed=11)[1]   # right eye of frame 0
+    img = P.render_forward(sc, c.width, c.height, view=v)
+    ref = oracle.render_forward(view_scene(sc, v), c.width, c.height)
+    assert_forward_matches(img.numpy(), {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)}, "c4")
     refup = oracle.upscale_spline(ref.color, ref.d_dx, ref.d_dy, ref.d_dxdy, c.factor)
     pipe = ViewPipeline(sc, c.width, c.height, factor=c.factor, slots=1)
     up = pipe.render([v], keep=True)[0].cpu().numpy()
