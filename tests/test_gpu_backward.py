@@ -94,3 +94,22 @@ def test_backward_matches_oracle_c5_scale(P, oracle):
     for f in FIELDS:
         err = rel_err(grads[f], ref[f])
         assert err < 1e-3, (f, err)
+
+
+def test_training_forward_matches_oracle_c5_full_size(P, oracle):
+    """C5 at full size (1M splats on the 1920x1080 canvas, one bench view rendered at
+    480x270 in training mode, i.e. with the float64 A-state), then the x4 upscale to
+    1920x1080: contrib_count bit-exact, planes and the upscaled frame <= 1e-4."""
+    from paper_2503_14171_b200.scenes import CONFIGS, random_views, synthetic_scene, view_scene
+    c = CONFIGS["c5"]
+    sc = synthetic_scene(c.n, c.canvas_w, c.canvas_h, c.scale_range, seed=5)
+    v = random_views(8, c.canvas_w, c.canvas_h, seed=13)[5]
+    img = P.render_forward(sc, c.width, c.height, view=v, train=True)
+    ref = oracle.render_forward(view_scene(sc, v), c.width, c.height)
+    got = img.numpy()
+    assert np.array_equal(got["contrib_count"], ref.contrib_count)
+    for f in ("color", "d_dx", "d_dy", "d_dxdy", "alpha", "alpha_dx", "alpha_dy", "alpha_dxdy"):
+        assert np.abs(got[f] - getattr(ref, f)).max() < 1e-4, f
+    up = P.upscale_spline(img, 4.0, out_size=c.out_size).cpu().numpy()
+    refup = oracle.upscale_spline(ref.color, ref.d_dx, ref.d_dy, ref.d_dxdy, 4.0, out_size=c.out_size)
+    assert np.abs(up - refup).max() < 1e-4
