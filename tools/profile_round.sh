@@ -18,6 +18,9 @@ for k in raster_fwd_kernel upscale_x4_kernel fill_rows_kernel preprocess_kernel 
     timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
         -o $O/ncu_$k $CMD > /dev/null 2>&1; echo "ncu $k rc=$?"
 done
+CMD4="python bench.py --config c4 --views 4 --kernel-views 4 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:upscale_x2_kernel -s 3 -c 1 \
+    -o $O/ncu_upscale_x2_kernel $CMD4 > /dev/null 2>&1; echo "ncu upscale_x2 rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"raster_bwd_kernel|ssim_stats|ssim_grad|upscale_bwd" -s 4 -c 4 \
     -o $O/ncu_train python tools/kprof_train.py 1 1 > /dev/null 2>&1; echo "ncu train rc=$?"
 ls -la $O
