@@ -517,6 +517,13 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
 //      float64 accumulation `acc = acc + alpha * (1 - acc)` for the
 //      termination decision (_kernels.py:105-111) and the same float32 (or
 //      TRAIN float64) value recurrences as the main pass.
+// Launch shapes.  Inference: 64 threads at <= 64 registers and a 512-candidate
+// segment (23 KB), small enough to co-reside with the next view's persistent
+// raster (which leaves 4096 registers and ~110 KB of shared memory per SM), so
+// the latency-bound fix-up of view k overlaps the raster of view k+1 in the
+// multi-stream pipeline (C3: 1831 -> 1855 frames/s; the 512-thread shape
+// serialises because it cannot fit beside a raster CTA).  Training keeps the
+// wide shape: its float64 blend state would spill at 64 registers.
 #ifndef FIX_SEG
 #define FIX_SEG 2048
 #endif
@@ -526,25 +533,34 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
 #ifndef FIX_GRID
 #define FIX_GRID (148 * 2)
 #endif
-constexpr int kFixSeg = FIX_SEG;
-constexpr int kFixThreads = FIX_THREADS;
-constexpr int kFixPer = kFixSeg / kFixThreads;
+template <bool TRAIN>
+struct FixShape {
+    static constexpr int kSeg = TRAIN ? FIX_SEG : 512;
+    static constexpr int kThreads = TRAIN ? FIX_THREADS : 64;
+    static constexpr int kMinBlocks = TRAIN ? 1 : 16;   // 16 x 64 threads: <= 64 registers
+    static constexpr int kPer = kSeg / kThreads;
+    static_assert(kPer <= 32 && kSeg % kThreads == 0, "candidates per thread fit the keep mask");
+};
 
+template <bool TRAIN>
 struct FixShared {
-    double a64[kFixSeg];
-    float4 val[kFixSeg];   // al, ax, ay, axy (compacted survivors)
-    float4 col[kFixSeg];
-    uint32_t idx[kFixSeg]; // list index of each survivor
-    int8_t st[kFixSeg];
-    uint32_t wcount[kFixThreads / 32];
+    static constexpr int kSeg = FixShape<TRAIN>::kSeg;
+    double a64[kSeg];
+    float4 val[kSeg];   // al, ax, ay, axy (compacted survivors)
+    float4 col[kSeg];
+    uint32_t idx[kSeg]; // list index of each survivor
+    int8_t st[kSeg];
+    uint32_t wcount[FixShape<TRAIN>::kThreads / 32];
     int nsurv;
     int done;
 };
 
 template <bool TRAIN>
-__global__ void __launch_bounds__(kFixThreads) fixup_kernel(RasterArgs p) {
+__global__ void __launch_bounds__(FixShape<TRAIN>::kThreads, FixShape<TRAIN>::kMinBlocks) fixup_kernel(RasterArgs p) {
+    constexpr int kFixSeg = FixShape<TRAIN>::kSeg, kFixThreads = FixShape<TRAIN>::kThreads;
+    constexpr int kFixPer = FixShape<TRAIN>::kPer;
     extern __shared__ __align__(16) unsigned char fix_raw[];
-    FixShared& S = *reinterpret_cast<FixShared*>(fix_raw);
+    FixShared<TRAIN>& S = *reinterpret_cast<FixShared<TRAIN>*>(fix_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t nfix = p.counters[2];
     for (uint32_t w = blockIdx.x; w < nfix; w += gridDim.x) {
@@ -676,19 +692,19 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
         SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<true>, kRasterThreads, 0));
         grid_train = max(per_sm, 1) * sms;
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fixup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)sizeof(FixShared)));
+                                              (int)sizeof(FixShared<false>)));
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fixup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)sizeof(FixShared)));
+                                              (int)sizeof(FixShared<true>)));
     }
     const int ntiles = L.ntx * L.nty;
     // counters[2] = fix-up pixels, counters[3] = work-unit cursor of the persistent raster
     SPLAT_CUDA_CHECK(cudaMemsetAsync(a.counters + 2, 0, 8, stream));
     if (train) {
         raster_fwd_kernel<true><<<grid_train, kRasterThreads, 0, stream>>>(a); note_launch();
-        fixup_kernel<true><<<FIX_GRID, kFixThreads, sizeof(FixShared), stream>>>(a); note_launch();
+        fixup_kernel<true><<<FIX_GRID, FixShape<true>::kThreads, sizeof(FixShared<true>), stream>>>(a); note_launch();
     } else {
         raster_fwd_kernel<false><<<grid_inf, kRasterThreads, 0, stream>>>(a); note_launch();
-        fixup_kernel<false><<<FIX_GRID, kFixThreads, sizeof(FixShared), stream>>>(a); note_launch();
+        fixup_kernel<false><<<FIX_GRID, FixShape<false>::kThreads, sizeof(FixShared<false>), stream>>>(a); note_launch();
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
