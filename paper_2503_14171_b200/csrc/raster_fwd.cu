@@ -211,7 +211,7 @@ __device__ __forceinline__ void write_pixel(const RasterArgs& p, int px, int py,
     p.alpha[2 * P + o] = sy;
     p.alpha[3 * P + o] = sxy;
     p.count[o] = s.n;
-    p.last[o] = s.last;
+    if (TRAIN) p.last[o] = s.last;
     if (TRAIN) {
         double2* st = reinterpret_cast<double2*>(p.state + 4 * o);
         st[0] = make_double2(s.Td, s.axd);
@@ -264,7 +264,7 @@ __device__ __forceinline__ void apply_candidate(int st, float al, float gax, flo
     else s.err = fmaf(-s.err, al, fmaf(s.T * al, rel, s.err));   // err (1 - al) + ta rel, no om
     if (TRAIN) s.add(al, gax, gay, gaxy, om, col);
     else s.add_raw(al, gax, gay, gaxy, col);
-    s.last = j + 1;
+    if (TRAIN) s.last = j + 1;   // contributor-list end: the backward's replay start (training only)
     // err stays far below 1e-6 (flagged pixels stop), so T > 1.02e-4 is never a decision.
     const float T = s.T;
     if (T <= 1.02e-4f) {
