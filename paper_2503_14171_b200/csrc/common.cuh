@@ -35,7 +35,10 @@ struct SceneConst {
 struct __align__(16) PackF {
     float mxh, myh, mxl, myl;     // render-space mean as float hi + lo parts ((x, y) pairs for FADD2)
     float a, c, b, sigma;         // conic (a, c adjacent for FMUL2) and opacity
-    float qcull, qclamp, pad0, pad1;  // ln(255 sigma), ln(sigma / 0.999), b/a, b/c
+    // decision thresholds of eval_fast with its qcull-relative tolerance folded in (directed
+    // rounding): qcull (1 + 2^-19) up, qcull (1 - 2^-19) down, qclamp + 2^-19 qcull up,
+    // qclamp - 2^-19 qcull down; qcull = ln(255 sigma), qclamp = ln(sigma / 0.999)
+    float cull_hi, cull_lo, clamp_hi, clamp_lo;
     float ex, ey, pad2, pad3;     // half extents of the cull ellipse; pad2: 4x2-group Q-norm bound (pre-filters only)
 };
 

@@ -119,16 +119,18 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
     float t3 = t13.y;
     float qf = (t1 + t2) + t3;
     float s = (t1 + fabsf(t2)) + t3;
-    // |qf - Q_exact| <= ~8 ulp * s; conic/mean rounding adds ~4 ulp * s.  2^-19 * s is a 2x margin.
-    // (tol = 0 only when s + qcull = 0, where every test below is "unsure")
-    float tol = (s + g.qcull) * 1.9073486e-06f;
+    // |qf - Q_exact| <= ~8 ulp * s; conic/mean rounding adds ~4 ulp * s.  2^-19 * s is a 2x margin
+    // (the one rounding of lo/hi below adds <= 0.5 ulp * s).  The tests are qf -+ tol against the
+    // thresholds with tol = (s + qcull) 2^-19; the qcull part is folded into the pack's
+    // outward-rounded cull_hi/lo, clamp_hi/lo.  (s + qcull = 0: every test below is "unsure".)
+    const float lo = fmaf(s, -1.9073486e-06f, qf), hi = fmaf(s, 1.9073486e-06f, qf);
     // |al - alpha_ref| / al <= 2^-21 s (Q) + 2^-20 (exp2 approx, log2e product, sigma, product);
     // + 2^-24 for the extra rounding of t al in the forward's T' = T - t al
     rel = fmaf(s, 4.7683716e-07f, 1.0132790e-06f);
-    if (qf > g.qcull + tol) return kCulled;
-    if (qf >= g.qcull - tol) return kUnsure;
-    if (qf <= g.qclamp + tol) {
-        if (qf < g.qclamp - tol) {
+    if (lo > g.cull_hi) return kCulled;
+    if (hi >= g.cull_lo) return kUnsure;
+    if (lo <= g.clamp_hi) {
+        if (hi < g.clamp_lo) {
             al = 0.999f;
             ax = 0.f;
             ay = 0.f;
@@ -216,12 +218,15 @@ __device__ __forceinline__ uint32_t group_qnorm_mask(const PackF& g, float X0, f
 // is a 1-D quadratic minimised in closed form.  Each edge value is lowered by
 // a bound on its float32 error (2^-18 (a u^2 + c v^2) >= 8 ulp * s) before the
 // comparison, and NaNs keep the candidate, so no contributing candidate is
-// ever rejected.  pad0/pad1 of the pack hold b/a and b/c.
+// ever rejected.  cull_hi >= qcull keeps the test conservative; b/a and b/c are
+// approximate quotients (a perturbed edge minimiser only raises the edge value by O(eps^2),
+// far inside the 2^-18 margin).
 __device__ __forceinline__ bool ellipse_hits_rect(const PackF& g, float X0, float X1, float Y0, float Y1) {
     const float u0 = (X0 - g.mxh) - g.mxl, u1 = (X1 - g.mxh) - g.mxl;
     const float v0 = (Y0 - g.myh) - g.myl, v1 = (Y1 - g.myh) - g.myl;
     if (u0 <= 0.f && u1 >= 0.f && v0 <= 0.f && v1 >= 0.f) return true;
     const float b2 = 2.f * g.b;
+    const float ba = __fdividef(g.b, g.a), bc = __fdividef(g.b, g.c);
     float lo = 3.0e38f;
     auto edge = [&](float u, float v) {
         float t1 = (g.a * u) * u, t3 = (g.c * v) * v;
@@ -229,12 +234,12 @@ __device__ __forceinline__ bool ellipse_hits_rect(const PackF& g, float X0, floa
         lo = fminf(lo, fmaf(-(t1 + t3), 3.8146973e-06f, qv));
     };
     // vertical edges u = u0, u1: v* = -(b/c) u clamped
-    edge(u0, fminf(fmaxf(-g.pad1 * u0, v0), v1));
-    edge(u1, fminf(fmaxf(-g.pad1 * u1, v0), v1));
+    edge(u0, fminf(fmaxf(-bc * u0, v0), v1));
+    edge(u1, fminf(fmaxf(-bc * u1, v0), v1));
     // horizontal edges v = v0, v1: u* = -(b/a) v clamped
-    edge(fminf(fmaxf(-g.pad0 * v0, u0), u1), v0);
-    edge(fminf(fmaxf(-g.pad0 * v1, u0), u1), v1);
-    return !(lo > fmaf(g.qcull, 3.8146973e-06f, g.qcull));
+    edge(fminf(fmaxf(-ba * v0, u0), u1), v0);
+    edge(fminf(fmaxf(-ba * v1, u0), u1), v1);
+    return !(lo > fmaf(g.cull_hi, 3.8146973e-06f, g.cull_hi));
 }
 
 }  // namespace

@@ -116,14 +116,21 @@ __global__ void preprocess_kernel(SceneConst sc, ViewConst vc, int width, int he
     p.b = (float)b;
     p.c = (float)c;
     p.sigma = (float)sg;
-    p.qcull = (float)q;
-    // ln(sigma / 0.999) in float32 (<= 2 ulp): eval_fast's tolerance carries a qcull-relative
-    // term of 2^-19 qcull >= 16 ulp(qclamp) (qclamp < qcull), so the clamp decision stays certified
-    p.qclamp = logf(p.sigma / (float)kAlphaClamp);
-    // ellipse-rectangle test: edge minimisers (a perturbed minimiser only raises the edge
-    // value by O(eps^2), far inside that test's 2^-18 margin)
-    p.pad0 = p.b / p.a;
-    p.pad1 = p.b / p.c;
+    // eval_fast's tests qf > qcull + tol etc. with tol = (s + qcull) 2^-19 become
+    // qf - 2^-19 s > cull_hi etc.: the qcull-relative part of the tolerance is added here
+    // exactly (double) and rounded outward, so the float32 path does one FMA per side.
+    // qcull and qclamp are the float32 values the tolerance was designed around (qclamp:
+    // ln(sigma / 0.999) in float32, <= 2 ulp; 2^-19 qcull >= 16 ulp(qclamp) when clamping
+    // is possible, qclamp < qcull).
+    {
+        const float qc = (float)q;
+        const float ql = logf(p.sigma / (float)kAlphaClamp);
+        const double tq = (double)qc * 1.9073486328125e-06;   // 2^-19 qcull, exact
+        p.cull_hi = __double2float_ru((double)qc + tq);
+        p.cull_lo = __double2float_rd((double)qc - tq);
+        p.clamp_hi = __double2float_ru((double)ql + tq);
+        p.clamp_lo = __double2float_rd((double)ql - tq);
+    }
     // cull-ellipse half extents (the reference's rx, ry) with a 1e-3 px + 1e-5 relative
     // margin: every pixel centre that can contribute lies in mean +- (ex, ey)
     p.ex = (float)(rx * (1.0 + 1e-5) + 1e-3);
