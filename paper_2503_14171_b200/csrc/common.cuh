@@ -34,7 +34,7 @@ struct SceneConst {
 // Per-view float32 pack the rasterizer consumes (rank order, 64 bytes).
 struct __align__(16) PackF {
     float mxh, myh, mxl, myl;     // render-space mean as float hi + lo parts ((x, y) pairs for FADD2)
-    float a, c, b, sigma;         // conic (a, c adjacent for FMUL2) and opacity
+    float a, c, nb2, l2sig;       // conic a, c (adjacent for FMUL2), nb2 = -2 b (exact), log2(sigma)
     // decision thresholds of eval_fast with its qcull-relative tolerance folded in (directed
     // rounding): qcull (1 + 2^-19) up, qcull (1 - 2^-19) down, qclamp + 2^-19 qcull up,
     // qclamp - 2^-19 qcull down; qcull = ln(255 sigma), qclamp = ln(sigma / 0.999)

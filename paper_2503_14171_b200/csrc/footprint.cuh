@@ -112,10 +112,9 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
     const float dx = d.x, dy = d.y;
     const float2 acd = fmul2(make_float2(g.a, g.c), d);
     const float adx = acd.x;
-    float b2 = 2.f * g.b;
     const float2 t13 = fmul2(acd, d);   // (a dx dx, c dy dy)
     float t1 = t13.x;
-    float t2 = (b2 * dx) * dy;
+    float t2 = ((-g.nb2) * dx) * dy;   // (2b dx) dy
     float t3 = t13.y;
     float qf = (t1 + t2) + t3;
     float s = (t1 + fabsf(t2)) + t3;
@@ -124,7 +123,8 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
     // thresholds with tol = (s + qcull) 2^-19; the qcull part is folded into the pack's
     // outward-rounded cull_hi/lo, clamp_hi/lo.  (s + qcull = 0: every test below is "unsure".)
     const float lo = fmaf(s, -1.9073486e-06f, qf), hi = fmaf(s, 1.9073486e-06f, qf);
-    // |al - alpha_ref| / al <= 2^-21 s (Q) + 2^-20 (exp2 approx, log2e product, sigma, product);
+    // |al - alpha_ref| / al <= 2^-21 s (Q) + 2^-20 (exp2 approx 2^-22; rounding of the
+    // argument, of log2(e) and of log2(sigma), each <= 2^-22 absolute for |argument| <= 8);
     // + 2^-24 for the extra rounding of t al in the forward's T' = T - t al
     rel = fmaf(s, 4.7683716e-07f, 1.0132790e-06f);
     if (lo > g.cull_hi) return kCulled;
@@ -142,18 +142,18 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
         }
         return kUnsure;
     }
-    al = g.sigma * fast_exp2(-1.44269504f * qf);
-    // (gx, gy) = -2 ((b dy, b dx) + (a dx, c dy))
-    const float2 gxy = fmul2(ffma2(make_float2(g.b, g.b), make_float2(dy, dx), acd), make_float2(-2.f, -2.f));
+    al = fast_exp2(fmaf(qf, -1.44269504f, g.l2sig));
+    // (gx, gy) = -2 ((b dy, b dx) + (a dx, c dy)) = (-2b) (dy, dx) + (-2) (a dx, c dy), bit for bit
+    const float2 gxy = ffma2(make_float2(g.nb2, g.nb2), make_float2(dy, dx), fmul2(acd, make_float2(-2.f, -2.f)));
     if (RAW) {
         ax = gxy.x;
         ay = gxy.y;
-        axy = fmaf(gxy.x, gxy.y, -b2);
+        axy = fmaf(gxy.x, gxy.y, g.nb2);
     } else {
         const float2 axy2 = fmul2(make_float2(al, al), gxy);
         ax = axy2.x;
         ay = axy2.y;
-        axy = al * fmaf(gxy.x, gxy.y, -b2);
+        axy = al * fmaf(gxy.x, gxy.y, g.nb2);
     }
     return kContrib;
 }
@@ -170,11 +170,11 @@ __device__ __forceinline__ void canonical_values(const PackF& g, float cx, float
     float dx = (cx - g.mxh) - g.mxl;
     float dy = (cy - g.myh) - g.myl;
     float adx = g.a * dx;
-    float b2 = 2.f * g.b;
+    const float b = -0.5f * g.nb2, b2 = -g.nb2;
     float qf = ((adx * dx) + ((b2 * dx) * dy)) + ((g.c * dy) * dy);
-    al = g.sigma * fast_exp2(-1.44269504f * qf);
-    float gx = -2.f * fmaf(g.b, dy, adx);
-    float gy = -2.f * fmaf(g.b, dx, g.c * dy);
+    al = fast_exp2(fmaf(qf, -1.44269504f, g.l2sig));
+    float gx = -2.f * fmaf(b, dy, adx);
+    float gy = -2.f * fmaf(b, dx, g.c * dy);
     if (RAW) {
         ax = gx;
         ay = gy;
@@ -199,7 +199,7 @@ __device__ __forceinline__ uint32_t group_qnorm_mask(const PackF& g, float X0, f
     const float2 dxs = make_float2(d0.x, d0.x + 4.f), dys = make_float2(d0.y, d0.y + 2.f);
     const float2 t1 = fmul2(fmul2(make_float2(g.a, g.a), dxs), dxs);
     const float2 t3 = fmul2(fmul2(make_float2(g.c, g.c), dys), dys);
-    const float2 bx = fmul2(make_float2(2.f * g.b, 2.f * g.b), dxs);
+    const float2 bx = fmul2(make_float2(-g.nb2, -g.nb2), dxs);
     // groups 0, 1 (row dys.x) and 2, 3 (row dys.y)
     const float2 s01 = fadd2(t1, make_float2(t3.x, t3.x));
     const float2 s23 = fadd2(t1, make_float2(t3.y, t3.y));
@@ -225,8 +225,8 @@ __device__ __forceinline__ bool ellipse_hits_rect(const PackF& g, float X0, floa
     const float u0 = (X0 - g.mxh) - g.mxl, u1 = (X1 - g.mxh) - g.mxl;
     const float v0 = (Y0 - g.myh) - g.myl, v1 = (Y1 - g.myh) - g.myl;
     if (u0 <= 0.f && u1 >= 0.f && v0 <= 0.f && v1 >= 0.f) return true;
-    const float b2 = 2.f * g.b;
-    const float ba = __fdividef(g.b, g.a), bc = __fdividef(g.b, g.c);
+    const float b2 = -g.nb2, b = -0.5f * g.nb2;
+    const float ba = __fdividef(b, g.a), bc = __fdividef(b, g.c);
     float lo = 3.0e38f;
     auto edge = [&](float u, float v) {
         float t1 = (g.a * u) * u, t3 = (g.c * v) * v;

@@ -113,9 +113,11 @@ __global__ void preprocess_kernel(SceneConst sc, ViewConst vc, int width, int he
     p.myh = (float)my;
     p.myl = (float)(my - (double)p.myh);
     p.a = (float)a;
-    p.b = (float)b;
+    p.nb2 = -2.f * (float)b;   // exact scaling of the float32 conic b
     p.c = (float)c;
-    p.sigma = (float)sg;
+    // al = 2^(log2 sigma - log2(e) qf): one FFMA + EX2 (the float32 rounding of log2 sigma,
+    // |log2 sigma| <= 8, is <= 2^-22 absolute, inside eval_fast's rel budget)
+    p.l2sig = (float)log2(sg);
     // eval_fast's tests qf > qcull + tol etc. with tol = (s + qcull) 2^-19 become
     // qf - 2^-19 s > cull_hi etc.: the qcull-relative part of the tolerance is added here
     // exactly (double) and rounded outward, so the float32 path does one FMA per side.
@@ -124,7 +126,7 @@ __global__ void preprocess_kernel(SceneConst sc, ViewConst vc, int width, int he
     // is possible, qclamp < qcull).
     {
         const float qc = (float)q;
-        const float ql = logf(p.sigma / (float)kAlphaClamp);
+        const float ql = logf((float)sg / (float)kAlphaClamp);
         const double tq = (double)qc * 1.9073486328125e-06;   // 2^-19 qcull, exact
         p.cull_hi = __double2float_ru((double)qc + tq);
         p.cull_lo = __double2float_rd((double)qc - tq);

@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                     const float abar_xy = (abxyp.x + abxyp.y) + w[11] * u0;
                     if (st != kClamped) {   // _kernels.py:291-336
                         const float dx = (cx - g.mxh) - g.mxl, dy = (cy - g.myh) - g.myl;
-                        const float ca = g.a, cb = g.b, ccn = g.c;
+                        const float ca = g.a, cb = -0.5f * g.nb2, ccn = g.c;
                         const float gx = -(2.f * ca * dx + 2.f * cb * dy);
                         const float gy = -(2.f * cb * dx + 2.f * ccn * dy);
                         const float hxy = gx * gy - 2.f * cb;
