@@ -609,22 +609,25 @@ __global__ void __launch_bounds__(32 * UP_X4_WARPS, UP_X4_MINB) upscale_x4_kerne
 // then runs in registers.  A CTA = 8 warps = 8 cell rows x 32 groups (16 x 128
 // output pixels); persistent, TMA-staged source double buffer, TMA bulk stores.
 constexpr int kX2Groups = 32;
-constexpr int kX2CellRows = 8;
+#ifndef UP_X2_WARPS
+#define UP_X2_WARPS 8
+#endif
+constexpr int kX2CellRows = UP_X2_WARPS;   // cell rows per tile = warps per CTA
 constexpr int kX2SpanC = 2 * kX2Groups + 2;   // corner columns 2 g0 - 1 .. 2 g0 + 64
 constexpr int kX2SpanR = kX2CellRows + 1;
 #ifndef UP_X2_MINB
-#define UP_X2_MINB 2
+#define UP_X2_MINB (UP_X2_WARPS == 1 ? 14 : 2)
 #endif
 
 template <bool CLAMP>
-__global__ void __launch_bounds__(256, UP_X2_MINB) upscale_x2_kernel(const float* __restrict__ src, int in_w,
+__global__ void __launch_bounds__(32 * UP_X2_WARPS, UP_X2_MINB) upscale_x2_kernel(const float* __restrict__ src, int in_w,
                                                                      int in_h, float* __restrict__ out,
                                                                      int out_w, int out_h) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[2];
     constexpr size_t kStage = (size_t)kX2SpanR * kX2SpanC * 12;
     float* const s_src0 = reinterpret_cast<float*>(smem);
-    float4* const s_xp = reinterpret_cast<float4*>(s_src0 + 2 * kStage);  // 8 warps x 2 x 96 float4
+    float4* const s_xp = reinterpret_cast<float4*>(s_src0 + 2 * kStage);  // warps x 2 x 96 float4
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ngx = (out_w / 4 + kX2Groups - 1) / kX2Groups;
     const int ngy = (in_h + 1 + kX2CellRows - 1) / kX2CellRows;   // cell rows -1 .. in_h-1
@@ -1104,13 +1107,13 @@ static int upscale_x4_launch(const float* src, int in_w, int in_h, float* out, i
 template <bool CLAMP>
 static int upscale_x2_launch(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
                              cudaStream_t stream) {
-    const size_t smem = 2 * (size_t)kX2SpanR * kX2SpanC * 48 + 8 * 2 * 96 * 16;
+    const size_t smem = 2 * (size_t)kX2SpanR * kX2SpanC * 48 + kX2CellRows * 2 * 96 * 16;
     static int per_sm = 0, sms = 0;
     if (!per_sm) {
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_x2_kernel<CLAMP>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         SPLAT_CUDA_CHECK(
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_x2_kernel<CLAMP>, 256, smem));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_x2_kernel<CLAMP>, 32 * kX2CellRows, smem));
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1118,7 +1121,8 @@ static int upscale_x2_launch(const float* src, int in_w, int in_h, float* out, i
     }
     const int ntiles = ceil_div(out_w / 4, kX2Groups) * ceil_div(in_h + 1, kX2CellRows);
     const int grid = max(1, min(ntiles, per_sm * sms));
-    upscale_x2_kernel<CLAMP><<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h); note_launch();
+    upscale_x2_kernel<CLAMP><<<grid, 32 * kX2CellRows, smem, stream>>>(src, in_w, in_h, out, out_w, out_h);
+    note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }
