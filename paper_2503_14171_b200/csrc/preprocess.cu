@@ -182,10 +182,16 @@ __global__ void pack64_kernel(SceneConst sc, ViewConst vc, double* __restrict__ 
 // Tile grids too large for the shared-memory tables fall back to per-pair
 // global atomics + a per-tile sort (same result).
 
-constexpr int kBinBlock = 4096;      // ranks per block (a histogram row)
+#ifndef BIN_BLOCK
+#define BIN_BLOCK 4096
+#endif
+#ifndef BIN_STAGE
+#define BIN_STAGE 16384
+#endif
+constexpr int kBinBlock = BIN_BLOCK;   // ranks per block (a histogram row)
 constexpr int kBinThreads = 1024;    // kBinBlock / kBinThreads ranks per thread
 constexpr int kBinRPT = kBinBlock / kBinThreads;
-constexpr int kBinStage = 16384;     // staged pairs per pass of the fill (2 CTAs/SM fit)
+constexpr int kBinStage = BIN_STAGE;   // staged pairs per pass of the fill (2 CTAs/SM fit)
 constexpr int kColGroup = 16;        // rows per column-scan group
 constexpr int kBinSmemMax = 200 * 1024;
 
