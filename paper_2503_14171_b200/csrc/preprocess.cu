@@ -76,6 +76,9 @@ __device__ __forceinline__ int64_t clip64(int64_t v, int64_t lo, int64_t hi) {
     return v < lo ? lo : (v > hi ? hi : v);
 }
 
+#ifndef PACK_ALL
+#define PACK_ALL 0
+#endif
 #ifndef PRE_THREADS
 #define PRE_THREADS 64   // 64 x 46 registers fit beside a persistent raster CTA set (C3 1896 -> 1911 frames/s)
 #endif
@@ -150,7 +153,13 @@ __global__ void __launch_bounds__(PRE_THREADS) preprocess_kernel(SceneConst sc, 
         p.pad2 = (float)(rt * rt * (1.0 + 1e-5) + 1e-4);
     }
     p.pad3 = 0.f;
+    // only splats that reach a tile list are ever read through the pack (raster, fix-up,
+    // backward): off-screen / culled splats skip the 64-byte store
+#if PACK_ALL
     pack[r] = p;
+#else
+    if (cnt != 0) pack[r] = p;
+#endif
 }
 
 
