@@ -10,6 +10,10 @@ A step renders + upscales every view of this rank's shard.
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
         torchrun --nproc-per-node N bench.py --gpus N ...
 
+Without torchrun, ``--gpus N`` (N > 1) launches the N ranks itself through
+torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1); under
+torchrun, a WORLD_SIZE different from --gpus is refused.
+
 Rank 0 prints ONE JSON line.
 """
 
@@ -56,7 +60,93 @@ def parse():
     ap.add_argument("--train-views", type=int, default=4, help="views per rank per training step (C5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: tests with several ranks on one GPU)")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="map ranks onto the visible GPUs modulo their count (multi-rank tests on one GPU; "
+                         "never a timing configuration)")
+    ap.add_argument("--shard-log", default=None,
+                    help="each rank writes the batch indices of its shard to <path>.<rank> (tests)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch/shard only: join the (gloo) group, write --shard-log, exit (no GPU; tests)")
     return ap.parse_args()
+
+
+def maybe_spawn(args) -> None:
+    """--gpus N without a torchrun environment: launch the N ranks through
+    torch.distributed.run and exit with its status.  Under torchrun the world
+    size must equal --gpus (a line whose n_gpus differs from --gpus is never printed)."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}: refusing a mismatched run")
+        return
+    if args.gpus <= 1 or args.impl == "reference":   # the reference arm runs on rank 0 alone
+        return
+    from paper_2503_14171_b200.distributed import free_port
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def setup_rank(args):
+    """(rank, world, device) of this process; joins the process group for N > 1."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world != max(args.gpus, 1):
+        sys.exit(f"bench.py: --gpus {args.gpus} but world size {world}")
+    ndev = torch.cuda.device_count()
+    if ndev < 1:
+        sys.exit("bench.py: no CUDA device visible")
+    if args.shared_gpu:
+        dev = local % ndev
+    elif local >= ndev:
+        sys.exit(f"bench.py: rank {rank} needs GPU {local} but only {ndev} are visible "
+                 "(--gpus must not exceed the GPU count)")
+    else:
+        dev = local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(args.dist_backend)
+    return rank, world, dev
+
+
+def dry_run(args) -> None:
+    """The launch and sharding logic of the render path without a GPU: every rank
+    joins a gloo group, computes its shard of the batch, logs it, and checks that
+    the whole job covers the batch exactly once."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world != max(args.gpus, 1):
+        sys.exit(f"bench.py: --gpus {args.gpus} but world size {world}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    nframes = args.views // views_per_frame(args)
+    lo, hi = frame_shard(nframes, views_per_frame(args), rank, world)
+    if args.shard_log:
+        with open(f"{args.shard_log}.{rank}", "w") as f:
+            json.dump({"rank": rank, "world": world, "lo": lo, "hi": hi}, f)
+    from paper_2503_14171_b200 import distributed as D
+    total = D.total_items(hi - lo)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "views": total}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def frame_shard(nframes: int, vpf: int, rank: int, world: int):
+    """[lo, hi) view indices of this rank: a contiguous, balanced run of whole frames
+    (both eyes of a stereo frame stay on one rank)."""
+    from paper_2503_14171_b200.distributed import shard_bounds
+    lo, hi = shard_bounds(nframes, rank, world)
+    return lo * vpf, hi * vpf
 
 
 def dist_env():
@@ -249,10 +339,7 @@ def run_train(args):
     from paper_2503_14171_b200 import _lib, distributed as D, fit
     from paper_2503_14171_b200.raster_forward import render_forward
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local = setup_rank(args)
     lib = _lib.load()
     vpr = args.train_views
     c, model, target_scene, views = train_workload(vpr, world)
@@ -379,10 +466,14 @@ def run_train(args):
 
 def main():
     args = parse()
+    maybe_spawn(args)
     if args.views is None:
         args.views = {"c2": 256, "c3": 1024, "c4": 64}[args.config]
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.dry_run:
+        dry_run(args)
         return
     if args.workload == "train":
         run_train(args)
@@ -390,12 +481,9 @@ def main():
     import torch
     import torch.distributed as dist
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local = setup_rank(args)
     import numpy as np
-    from paper_2503_14171_b200 import _lib
+    from paper_2503_14171_b200 import _lib, distributed as D
     from paper_2503_14171_b200.device import DeviceScene
     from paper_2503_14171_b200.pipeline import ViewPipeline
 
@@ -406,8 +494,15 @@ def main():
     vpf = views_per_frame(args)
     scene, views = make_workload(args)
     nframes = len(views) // vpf
-    per = (nframes + world - 1) // world * vpf    # shard whole frames (both eyes on one rank)
-    mine = views[rank * per:(rank + 1) * per]
+    lo, hi = frame_shard(nframes, vpf, rank, world)
+    mine = views[lo:hi]
+    if args.shard_log:
+        with open(f"{args.shard_log}.{rank}", "w") as f:
+            json.dump({"rank": rank, "world": world, "device": local, "lo": lo, "hi": hi,
+                       "views": [[v.zoom, v.ox, v.oy] for v in mine]}, f)
+    # pinned host buffers (e2e ring, scene upload) on the GPU's own NUMA node
+    numa = D.numa_node_of(local)
+    cpus = D.bind_host_to_numa(numa) if world > 1 else None
 
     pipe = ViewPipeline(scene, W, H, factor=F, slots=args.slots, views_for_capacity=mine)
 
@@ -467,11 +562,8 @@ def main():
     stage = kpipe.stage_times_ms()
     clk = clocks.stop()
     del kpipe
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    total_views = per * world if world > 1 else len(mine)
+    ms_max = D.max_over_ranks(ms, device="cuda")
+    total_views = D.total_items(len(mine), device="cuda")   # views rendered by the whole job
     value = total_views / vpf / (ms_max / 1e3)
 
     # ---- e2e through the public API with host buffers -------------------------------------
@@ -509,10 +601,8 @@ def main():
         p2.check()
         ems = s0.elapsed_time(s1) / ksteps
         wall = (time.perf_counter() - t0) / ksteps * 1e3
-        et = torch.tensor([max(ems, wall)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": total_views / vpf / (float(et.item()) / 1e3), "unit": "frames/s",
+        et = D.max_over_ranks(max(ems, wall), device="cuda")
+        e2e = {"value": total_views / vpf / (et / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": ksteps, "api": "DeviceScene upload + prepare, ViewPipeline.render(host_out=pinned ring)"}
 
@@ -567,11 +657,16 @@ def main():
                "sample": f"1 view of the {args.config.upper()} batch through the float64 oracle "
                          f"(render + x{F:g} upscale), x{vpf} views per frame"}
 
+    cfg = config_dict(args, world, len(mine))
+    if world > 1:
+        cfg["host_numa"] = {"node": numa, "cpus": len(cpus) if cpus else None,
+                            "note": "rank 0's pinned host ring is allocated on its GPU's NUMA node"}
+        cfg["backend"] = args.dist_backend
     if rank == 0:
         line = {"metric": metric_of(args), "value": value, "unit": "frames/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic", "config": config_dict(args, world, len(mine)),
+                "data": "synthetic", "config": cfg,
                 "mpix_per_s": value * vpf * OW * OH / 1e6,
                 "stage_ms_per_view": stage, "gpu_launches": int(launches),
                 "roofline": roof, "roofline_upscale": roof_up, "cpu_baseline": cpu, "e2e": e2e,

@@ -22,6 +22,16 @@ int set_cuda_error(cudaError_t e, const char* what) {
     return SPLAT_ERR_CUDA;
 }
 
+int device_sms(int& sms) {
+    static PerDevice<int> cache;
+    return cache.get(sms, [](int& v) {
+        int dev = 0;
+        SPLAT_CUDA_CHECK(cudaGetDevice(&dev));
+        SPLAT_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        return SPLAT_OK;
+    });
+}
+
 size_t scene_workspace_bytes_impl(int64_t n);
 int scene_prepare_impl(const splat_scene_t& s, void* const_buf, void* ws, cudaStream_t stream);
 int scene_refresh_impl(const splat_scene_t& s, void* const_buf, cudaStream_t stream);

@@ -1,6 +1,8 @@
 // Shared definitions for the sm_100a render + upscale kernels.
 #pragma once
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "../../include/splat_b200.h"
@@ -56,4 +58,41 @@ namespace splat {
 void note_launch();  // counts kernels launched by this library (splat_kernel_launches)
 int set_cuda_error(cudaError_t e, const char* what);
 int set_error(int code, const char* msg);
+
+// Launch configuration that is per device (the dynamic shared-memory opt-in of
+// cudaFuncSetAttribute, occupancy-derived grids, __constant__ tables): one
+// entry per device ordinal, initialised once under a mutex, so a process that
+// drives several GPUs, or calls from several host threads, configures each
+// device exactly once.  `init(T&)` returns SPLAT_OK or an error code.
+template <class T>
+class PerDevice {
+public:
+    template <class F>
+    int get(T& out, F&& init) {
+        int dev = 0;
+        SPLAT_CUDA_CHECK(cudaGetDevice(&dev));
+        if (dev < 0 || dev >= kMaxDevices) return set_error(SPLAT_ERR_PARAMETER, "device ordinal out of range");
+        if (!ready_[dev].load(std::memory_order_acquire)) {
+            std::lock_guard<std::mutex> lock(mu_);
+            if (!ready_[dev].load(std::memory_order_relaxed)) {
+                T v{};
+                const int rc = init(v);
+                if (rc != SPLAT_OK) return rc;
+                val_[dev] = v;
+                ready_[dev].store(true, std::memory_order_release);
+            }
+        }
+        out = val_[dev];
+        return SPLAT_OK;
+    }
+
+private:
+    static constexpr int kMaxDevices = 64;
+    std::atomic<bool> ready_[kMaxDevices] = {};
+    T val_[kMaxDevices] = {};
+    std::mutex mu_;
+};
+
+// SM count of the current device (cached per device).
+int device_sms(int& sms);
 }  // namespace splat

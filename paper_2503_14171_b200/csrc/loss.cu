@@ -355,8 +355,9 @@ size_t loss_workspace_bytes_impl(int w, int h) {
 
 int loss_impl(const float* pred, const float* target, int w, int h, double lam, float* adj, double* value,
               void* ws, cudaStream_t stream) {
-    static bool win_set = false;
-    if (!win_set) {
+    static PerDevice<bool> win_set;   // __constant__ tables and attributes are per device
+    bool ok = false;
+    const int rc = win_set.get(ok, [](bool& v) {
         double wd[11], sum = 0.0;
         for (int k = 0; k < 11; ++k) {
             const double x = k - 5;
@@ -372,8 +373,10 @@ int loss_impl(const float* pred, const float* target, int w, int h, double lam, 
         SPLAT_CUDA_CHECK(cudaMemcpyToSymbol(c_wind, wd, sizeof(wd)));
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(ssim_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)kStatsSmem));
-        win_set = true;
-    }
+        v = true;
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
     const int gx = ceil_div(w, kS), gy = ceil_div(h, kS);
     const size_t nparts = (size_t)gx * gy;
     float* coef = (float*)ws;

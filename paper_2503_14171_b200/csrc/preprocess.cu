@@ -824,16 +824,19 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
     const bool staged = ntiles <= 65535 && fill_smem <= kBinSmemMax && L.cap < 0xffffffffLL &&
                         !(flags & SPLAT_BIN_ATOMIC);
     if (staged) {
-        static bool configured = false;
-        if (!configured) {
+        static PerDevice<bool> configured;
+        bool ok = false;
+        const int rc = configured.get(ok, [](bool& v) {
             SPLAT_CUDA_CHECK(cudaFuncSetAttribute(count_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   kBinSmemMax));
             SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fill_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   kBinSmemMax));
             SPLAT_CUDA_CHECK(cudaFuncSetAttribute(colscan_groups_scan_kernel,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kScanTilesMax * 4));
-            configured = true;
-        }
+            v = true;
+            return SPLAT_OK;
+        });
+        if (rc != SPLAT_OK) return rc;
         uint32_t* hist = (uint32_t*)(ws + L.bin_hist);
         uint32_t* part = (uint32_t*)(ws + L.bin_part);
         const int grid = (int)(nrows < 148 * 2 ? nrows : 148 * 2);
@@ -870,12 +873,15 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         fill_tiles_kernel<<<blocks, 256, 0, stream>>>(L.n, bboxes, touched, L.ntx, L.cap, cursor, ranks, counters);
         note_launch();
     }
-    static bool configured = false;
-    if (!configured) {
+    static PerDevice<bool> configured;
+    bool ok = false;
+    const int rc = configured.get(ok, [](bool& v) {
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(segsort_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               kSegChunk * 4));
-        configured = true;
-    }
+        v = true;
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
     uint32_t* big = (uint32_t*)(ws + L.big_list);
     segsort_kernel<<<ntiles, kSegThreads, kSegSmall * 4, stream>>>(ntiles, ranges, ranks, keys, big, counters);
     note_launch();

@@ -369,7 +369,11 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
 #pragma unroll
             for (int i = 0; i < kG; ++i) S.part[slot][warp][lane][i] = acc[i];
         }
-        // publish; the last warp of the batch reduces the slot
+        // publish; the last warp of the batch reduces the slot.  Every lane fences its
+        // own partial stores and the warp converges before lane 0's release, so the
+        // partials are ordered before the `done` increment the reducer acquires.
+        __threadfence_block();
+        __syncwarp();
         int prev = 0;
         if (lane == 0) {
             S.touch[slot][warp] = touched;
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                     for (int i = 0; i < kG; ++i) dst[i] = acc[i];
                 }
             }
-            __syncwarp();
+            __syncwarp();   // every lane's reads of the slot precede its release
             if (lane == 0) {
                 S.done[slot] = 0;
                 __threadfence_block();
@@ -523,12 +527,15 @@ int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, con
     a.state = fwd.state;
     a.adj = adj;
     a.partial = partial;
-    static bool configured = false;
-    if (!configured) {
+    static PerDevice<bool> configured;
+    bool ok = false;
+    const int rc = configured.get(ok, [](bool& v) {
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)sizeof(BwdShared)));
-        configured = true;
-    }
+        v = true;
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
     raster_bwd_kernel<<<L.ntx * L.nty, kBlock, sizeof(BwdShared), stream>>>(a); note_launch();
     const int blocks = (int)((L.n + 255) / 256);
     TermScales ts;

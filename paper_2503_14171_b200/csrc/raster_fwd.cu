@@ -682,20 +682,27 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
     a.state = out.state;
     a.fixup = (uint32_t*)(ws + L.fixup);
     a.counters = (uint32_t*)(ws + L.counters);
-    static int grid_inf = 0, grid_train = 0;
-    if (!grid_inf) {
-        int per_sm = 0, dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    struct Grids {
+        int inf, train;
+    };
+    static PerDevice<Grids> grids;
+    Grids gr{};
+    const int rc = grids.get(gr, [](Grids& g) {
+        int per_sm = 0, sms = 148;
+        const int e = device_sms(sms);
+        if (e != SPLAT_OK) return e;
         SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<false>, kRasterThreads, 0));
-        grid_inf = max(per_sm, 1) * sms;
+        g.inf = max(per_sm, 1) * sms;
         SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<true>, kRasterThreads, 0));
-        grid_train = max(per_sm, 1) * sms;
+        g.train = max(per_sm, 1) * sms;
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fixup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)sizeof(FixShared<false>)));
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fixup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)sizeof(FixShared<true>)));
-    }
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
+    const int grid_inf = gr.inf, grid_train = gr.train;
     const int ntiles = L.ntx * L.nty;
     // counters[2] = fix-up pixels, counters[3] = work-unit cursor of the persistent raster
     SPLAT_CUDA_CHECK(cudaMemsetAsync(a.counters + 2, 0, 8, stream));

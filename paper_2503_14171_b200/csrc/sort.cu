@@ -281,13 +281,16 @@ template <typename K, int BITS>
 static int radix_pass(const K* src_k, const uint32_t* src_v, K* dst_k, uint32_t* dst_v, const uint32_t* n_dev,
                       int64_t n_host, int64_t cap, int shift, uint32_t* hist, uint32_t* hscan, int nb,
                       cudaStream_t stream) {
-    static bool configured = false;
-    if (!configured) {
+    static PerDevice<bool> configured;
+    bool ok = false;
+    const int rc = configured.get(ok, [](bool& v) {
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(radix_downsweep_kernel<K, BITS>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)downsweep_smem<K, BITS>()));
-        configured = true;
-    }
+        v = true;
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
     radix_upsweep_kernel<K, BITS><<<nb, kSortThreads, 0, stream>>>(src_k, n_dev, n_host, cap, shift, hist, nb); note_launch();
     exclusive_scan_u32(hist, hist, (int64_t)(1 << BITS) * nb, hscan, nullptr, stream);
     radix_downsweep_kernel<K, BITS><<<nb, kSortThreads, downsweep_smem<K, BITS>(), stream>>>(

@@ -1061,19 +1061,22 @@ static int upscale_int_launch(const float* src, int in_w, int in_h, float* out, 
     constexpr int TC = int_tile_cols(F);
     const int span_c = TC / F + 3, span_r = kUpRows / F + 3;
     const size_t smem = 2 * (size_t)span_r * span_c * 48 + (size_t)kUpRows * (TC / F + 2) * 24 + 8 * 96 * 16;
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
+    static PerDevice<int> slots;   // resident CTAs per device (attribute set once per device)
+    int cap = 0;
+    const int rc = slots.get(cap, [smem](int& v) {
+        int per_sm = 0, sms = 148;
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_int_kernel<F, CLAMP>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         SPLAT_CUDA_CHECK(
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_int_kernel<F, CLAMP>, 256, smem));
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (per_sm < 1) per_sm = 1;
-    }
+        const int e = device_sms(sms);
+        if (e != SPLAT_OK) return e;
+        v = max(per_sm, 1) * sms;
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
     const int ntiles = ceil_div(out_w, TC) * ceil_div(out_h, kUpRows);
-    const int grid = max(1, min(ntiles, per_sm * sms));
+    const int grid = max(1, min(ntiles, cap));
     upscale_int_kernel<F, CLAMP><<<grid, 256, smem, stream>>>(src, in_w, in_h, out, out_w, out_h, span_c,
                                                               span_r); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
@@ -1084,20 +1087,23 @@ template <bool CLAMP>
 static int upscale_x4_launch(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
                              cudaStream_t stream) {
     const size_t smem = 2 * (size_t)kX4SpanR * kX4SpanC * 48 + kX4CellRows * 96 * 16 * (UP_TMA_STORE ? 2 : 1);
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
+    static PerDevice<int> slots;
+    int cap = 0;
+    const int rc = slots.get(cap, [smem](int& v) {
+        int per_sm = 0, sms = 148;
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_x4_kernel<CLAMP>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_x4_kernel<CLAMP>,
                                                                        32 * kX4CellRows, smem));
         if (UP_X4_GRID_PER_SM > 0) per_sm = UP_X4_GRID_PER_SM;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (per_sm < 1) per_sm = 1;
-    }
+        const int e = device_sms(sms);
+        if (e != SPLAT_OK) return e;
+        v = max(per_sm, 1) * sms;
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
     const int ntiles = ceil_div(out_w / 4, kX4Groups) * ceil_div(in_h + 1, kX4CellRows);
-    const int grid = max(1, min(ntiles, per_sm * sms));
+    const int grid = max(1, min(ntiles, cap));
     upscale_x4_kernel<CLAMP><<<grid, 32 * kX4CellRows, smem, stream>>>(src, in_w, in_h, out, out_w, out_h);
     note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
@@ -1108,19 +1114,22 @@ template <bool CLAMP>
 static int upscale_x2_launch(const float* src, int in_w, int in_h, float* out, int out_w, int out_h,
                              cudaStream_t stream) {
     const size_t smem = 2 * (size_t)kX2SpanR * kX2SpanC * 48 + kX2CellRows * 2 * 96 * 16;
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
+    static PerDevice<int> slots;
+    int cap = 0;
+    const int rc = slots.get(cap, [smem](int& v) {
+        int per_sm = 0, sms = 148;
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_x2_kernel<CLAMP>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         SPLAT_CUDA_CHECK(
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_x2_kernel<CLAMP>, 32 * kX2CellRows, smem));
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (per_sm < 1) per_sm = 1;
-    }
+        const int e = device_sms(sms);
+        if (e != SPLAT_OK) return e;
+        v = max(per_sm, 1) * sms;
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
     const int ntiles = ceil_div(out_w / 4, kX2Groups) * ceil_div(in_h + 1, kX2CellRows);
-    const int grid = max(1, min(ntiles, per_sm * sms));
+    const int grid = max(1, min(ntiles, cap));
     upscale_x2_kernel<CLAMP><<<grid, 32 * kX2CellRows, smem, stream>>>(src, in_w, in_h, out, out_w, out_h);
     note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
@@ -1147,18 +1156,21 @@ int upscale_forward_impl(const float* src, int in_w, int in_h, float* out, int o
     if (span_r > in_h) span_r = in_h;
     size_t smem = 2 * (size_t)span_r * span_c * 48 + (size_t)kUpRows * span_c * 24 +
                   2 * ((size_t)tile_c * 20 + kUpRows * 20);
-    static int max_smem = 0;
-    if (!max_smem) {
+    static PerDevice<int> opt_in;
+    int max_smem = 0;
+    const int rc = opt_in.get(max_smem, [](int& v) {
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_fwd_kernel,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        max_smem = 220 * 1024;
-    }
+        v = 220 * 1024;
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
     if (smem > (size_t)max_smem) return set_error(SPLAT_ERR_DIMENSION, "upscale tile exceeds shared memory");
     int per_sm = 0;
     SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upscale_fwd_kernel, 256, smem));
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int sms = 148;
+    const int rs = device_sms(sms);
+    if (rs != SPLAT_OK) return rs;
     int ntiles = ceil_div(out_w, tile_c) * ceil_div(out_h, kUpRows);
     int grid = per_sm * sms;
     if (grid > ntiles) grid = ntiles;
@@ -1186,12 +1198,15 @@ int upscale_backward_impl(const float* adj, int out_w, int out_h, float* dsrc, i
         SPLAT_CUDA_CHECK(cudaGetLastError());
         return SPLAT_OK;
     }
-    static int configured = 0;
-    if (!configured) {
+    static PerDevice<bool> configured;
+    bool ok = false;
+    const int rc = configured.get(ok, [](bool& v) {
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               200 * 1024));
-        configured = 1;
-    }
+        v = true;
+        return SPLAT_OK;
+    });
+    if (rc != SPLAT_OK) return rc;
     if (smem > 200 * 1024) return set_error(SPLAT_ERR_DIMENSION, "upscale backward tile too large");
     dim3 grid(ceil_div(in_w, kBwCols), ceil_div(in_h, kBwRows));
     upscale_bwd_kernel<<<grid, 256, smem, stream>>>(adj, out_w, out_h, dsrc, in_w, in_h, sx, sy, max_u, max_v);

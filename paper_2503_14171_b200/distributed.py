@@ -16,6 +16,7 @@ on CPU (tests/test_distributed.py).
 from __future__ import annotations
 
 import os
+import socket
 
 import torch
 import torch.distributed as dist
@@ -64,3 +65,44 @@ def total_items(n_local: int, device=None, group=None) -> int:
     t = torch.tensor([int(n_local)], dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return int(t.item())
+
+
+def free_port() -> int:
+    """An unused TCP port on 127.0.0.1 for a local rendezvous."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def numa_node_of(device: int) -> int | None:
+    """NUMA node the GPU hangs off (sysfs), or None when unknown / single-node."""
+    try:
+        p = torch.cuda.get_device_properties(device)
+        path = f"/sys/bus/pci/devices/{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0/numa_node"
+        node = int(open(path).read().strip())
+        return node if node >= 0 else None
+    except Exception:
+        return None
+
+
+def bind_host_to_numa(node: int | None) -> list | None:
+    """Restrict this process's CPUs to ``node`` so pinned host buffers allocated
+    afterwards are first-touched (hence placed) on the GPU's own NUMA node.
+    Returns the CPU list, or None if nothing was changed."""
+    if node is None:
+        return None
+    try:
+        spec = open(f"/sys/devices/system/node/node{node}/cpulist").read().strip()
+        cpus = []
+        for part in spec.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.extend(range(int(lo), int(hi or lo) + 1))
+        cpus = [c for c in cpus if c in os.sched_getaffinity(0)]
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return cpus
+    except Exception:
+        return None

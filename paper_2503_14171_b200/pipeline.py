@@ -18,9 +18,10 @@ from __future__ import annotations
 import torch
 
 from . import _lib
+from .core import DimensionError
 from .device import to_device
 from .raster_forward import Frame, GradientImage, make_view
-from .spline import output_size, upscale_plan
+from .spline import check_output, output_size, upscale_plan
 
 STAGES = ("prepare", "bin", "raster", "upscale")
 
@@ -88,8 +89,16 @@ class ViewPipeline:
         """
         lib, ds = self.lib, self.scene
         kept = [] if keep else None
+        if out is not None:
+            if not torch.is_tensor(out) or out.dim() != 4 or out.shape[0] < len(views):
+                raise DimensionError("out must be a (V, Ho, Wo, 3) tensor with V >= len(views)")
+            for i in range(len(views)):
+                check_output(out[i], self.out_w, self.out_h, ds.device)
         if host_out is not None and self.copy_stream is None:
             self.copy_stream = torch.cuda.Stream(device=ds.device)
+        # every slot (and the copy stream) starts after the work the caller queued so far on
+        # its stream: the scene upload / prepare, the Frame counter zeroing, the upscale plan
+        self.fork()
         for i, v in enumerate(views):
             slot = self.slots[i % self.nslots]
             cv = make_view(ds, self.width, self.height, v)

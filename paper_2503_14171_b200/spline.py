@@ -21,7 +21,7 @@ from .core import DimensionError, UnsupportedScaleError
 from .raster_forward import GradientImage
 
 __all__ = ["upscale_spline", "upscale_backward", "SourceAdjoint", "fd_gradients",
-           "fd_gradients_backward", "output_size", "upscale_plan"]
+           "fd_gradients_backward", "output_size", "upscale_plan", "check_output"]
 
 
 def output_size(in_w: int, in_h: int, factor: float):
@@ -42,6 +42,24 @@ def _planes(img: GradientImage) -> torch.Tensor:
     if not p.is_contiguous():
         p = p.contiguous()
     return p
+
+
+def check_output(out: torch.Tensor, out_w: int, out_h: int, device) -> None:
+    """A caller-provided destination must be exactly what the kernels write:
+    (out_h, out_w, 3) float32, contiguous, on ``device``, and 16-byte aligned
+    when rows are written with 16-byte (TMA bulk / vector) stores, i.e. when
+    out_w % 4 == 0.  Anything else would be written out of bounds or fault."""
+    if not torch.is_tensor(out):
+        raise DimensionError("out must be a torch tensor")
+    if tuple(out.shape) != (out_h, out_w, 3):
+        raise DimensionError(f"out must have shape {(out_h, out_w, 3)}, got {tuple(out.shape)}")
+    if out.dtype != torch.float32:
+        raise DimensionError("out must be float32")
+    if out.device != torch.device(device):
+        raise DimensionError(f"out must be on {device}, got {out.device}")
+    align = 16 if out_w % 4 == 0 else 4
+    if not out.is_contiguous() or out.data_ptr() % align:
+        raise DimensionError(f"out must be contiguous and {align}-byte aligned")
 
 
 _plans: dict = {}
@@ -72,8 +90,12 @@ def upscale_spline(img, factor: float, *, out_size=None, clamp: bool = True,
             raise UnsupportedScaleError("output must be at least source size")
     lib = _lib.load()
     src = _planes(g)
+    if src.data_ptr() % 16:
+        src = src.clone()   # the source planes are staged with 16-byte bulk copies
     if out is None:
         out = torch.empty((out_h, out_w, 3), dtype=torch.float32, device=src.device)
+    else:
+        check_output(out, out_w, out_h, src.device)
     plan = upscale_plan(g.width, g.height, out_w, out_h, src.device)
     _lib.check(lib.splat_upscale_forward(_lib.ptr(src), g.width, g.height, _lib.ptr(out), out_w, out_h,
                                          int(bool(clamp)), _lib.ptr(plan), _lib.stream_ptr()))

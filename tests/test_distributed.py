@@ -71,3 +71,40 @@ def test_gloo_world2_views_and_allreduce():
     assert np.array_equal(g0, expect) and np.array_equal(g1, expect)   # identical update everywhere
     assert t0 == t1 == 2.0
     assert n0 == n1 == 10
+
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench(args, env=None, timeout=300):
+    import subprocess
+    import sys
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, capture_output=True,
+                          text=True, env=e, timeout=timeout, cwd=ROOT)
+
+
+@pytest.mark.parametrize("world,config,views", [(2, "c3", 1024), (3, "c3", 1024), (3, "c4", 64)])
+def test_bench_gpus_n_spawns_n_ranks_and_shards_the_batch(tmp_path, world, config, views):
+    """`bench.py --gpus N` outside torchrun launches N ranks itself; their shards
+    are disjoint, contiguous, balanced whole frames covering the batch once."""
+    log = str(tmp_path / "shard")
+    r = _bench(["--gpus", str(world), "--dry-run", "--config", config, "--views", str(views),
+                "--shard-log", log])
+    assert r.returncode == 0, r.stderr[-2000:]
+    import json
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == world and line["views"] == views
+    spans = sorted(tuple(json.load(open(f"{log}.{k}"))[x] for x in ("lo", "hi")) for k in range(world))
+    assert spans[0][0] == 0 and spans[-1][1] == views
+    assert all(b == c for (_, b), (c, _) in zip(spans, spans[1:]))
+    vpf = 2 if config == "c4" else 1
+    sizes = [(b - a) // vpf for a, b in spans]
+    assert all((b - a) % vpf == 0 for a, b in spans) and max(sizes) - min(sizes) <= 1
+
+
+def test_bench_refuses_a_world_size_other_than_gpus():
+    r = _bench(["--gpus", "2", "--dry-run"], env={"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and "refusing" in r.stderr
+    assert not any(ln.startswith("{") for ln in r.stdout.splitlines())

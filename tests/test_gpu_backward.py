@@ -22,6 +22,31 @@ def rel_err(got, ref):
     return float((np.abs(got - ref) / np.maximum(np.abs(ref), 1e-3 * scale)).max()) if ref.size else 0.0
 
 
+STRICT_FLOOR = 1e-6   # absolute floor of the strict check, relative to the field's max |ref|
+
+
+def strict_pass_fraction(got, ref, rtol=1e-3, floor=STRICT_FLOOR):
+    """Fraction of elements with |got - ref| <= rtol * max(|ref|, floor * max|ref|): the
+    reference's own per-element test (test_raster_backward.py:176-180, denominator
+    max(|ref|, 1e-6)) with its absolute 1e-6 floor made relative to the field's scale,
+    since the C5 gradients are ~1e-6 or smaller in absolute terms."""
+    if not ref.size:
+        return 1.0
+    scale = max(np.abs(ref).max(), 1e-30)
+    ok = np.abs(got - ref) <= rtol * np.maximum(np.abs(ref), floor * scale)
+    return float(ok.mean())
+
+
+def record(name, payload):
+    """Append a measured parity figure to gpurun_out/parity.jsonl (kept as evidence)."""
+    import json
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(root, "gpurun_out", "parity.jsonl"), "a") as f:
+        f.write(json.dumps({"test": name, **payload}) + "\n")
+
+
 @pytest.fixture(scope="module")
 def P():
     import paper_2503_14171_b200 as P
@@ -91,9 +116,13 @@ def test_backward_matches_oracle_c5_scale(P, oracle):
     grads = P.render_backward(sc, img, P.PixelAdjoint.of(*adjs)).numpy()
     ref_img = oracle.render_forward(sc, w, h)
     ref = oracle.render_backward(sc, ref_img, adjs)
+    strict = {f: strict_pass_fraction(grads[f], ref[f]) for f in FIELDS}
+    record("c5_100k_backward", {"strict_1e-3_pass_fraction": strict, "floor": STRICT_FLOOR,
+                                "field_rel_err": {f: rel_err(grads[f], ref[f]) for f in FIELDS}})
     for f in FIELDS:
         err = rel_err(grads[f], ref[f])
         assert err < 1e-3, (f, err)
+        assert strict[f] >= 0.999, (f, strict[f])
 
 
 def test_training_forward_matches_oracle_c5_full_size(P, oracle):
@@ -148,6 +177,17 @@ def test_training_step_gradients_match_oracle_c5_full_size(P, oracle):
     assert np.abs(a64 - ref_adj)[same].max() < 1e-4 * np.abs(ref_adj).max()
     ref = oracle.render_backward(sv, ref_img, oracle.upscale_backward(c.width, c.height, 4.0, a64,
                                                                       out_size=(W, H)))
+    strict = {f: strict_pass_fraction(grads[f], ref[f]) for f in FIELDS}
+    worst = {}
+    for f in FIELDS:
+        scale = np.abs(ref[f]).max()
+        e = np.abs(grads[f] - ref[f]) / np.maximum(np.abs(ref[f]), STRICT_FLOOR * scale)
+        worst[f] = {"max": float(e.max()), "p99.9": float(np.quantile(e, 0.999)),
+                    "failing": int((e > 1e-3).sum()), "n": int(e.size)}
+    record("c5_full_size_step", {"strict_1e-3_pass_fraction": strict, "floor": STRICT_FLOOR,
+                                 "strict_rel_err": worst,
+                                 "field_rel_err": {f: rel_err(grads[f], ref[f]) for f in FIELDS}})
     for f in FIELDS:
         err = rel_err(grads[f], ref[f])
         assert err < 1e-3, (f, err)
+        assert strict[f] >= 0.999, (f, strict[f])

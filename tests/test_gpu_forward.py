@@ -405,3 +405,96 @@ def test_termination_boundary_stress(P, oracle, seed, clamped):
     assert_forward_matches(got, {f: getattr(ref, f) for f in FIELDS + ("contrib_count",)}, f"shell{seed}")
     # the scene does exercise the exact fix-up of undecidable pixels
     assert img.stats.get("fixup_pixels", 0) > 0 or not clamped
+
+
+def _scale_case(cfg):
+    from paper_2503_14171_b200.scenes import CONFIGS, random_views, stereo_views, synthetic_scene
+    c = CONFIGS[cfg]
+    sc = synthetic_scene(c.n, c.width, c.height, c.scale_range, seed=5)
+    if cfg == "c3":
+        v = random_views(c.views, c.width, c.height, seed=11)[7]      # as bench.py's batch
+    elif cfg == "c4":
+        v = stereo_views(1, c.width, c.height, seed=11)[1]            # right eye of frame 0
+    else:
+        v = None
+    return c, sc, v
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_preprocess_and_binning_bitexact_at_config_scale(P, oracle, cfg):
+    """Integer parity at full config size (north_star: tile keys, sort order and per-tile
+    ranges bit-exact): the device's depth order, bboxes and validity (float64 expression
+    trees with libdevice exp/sin/cos/log vs numpy's) and the whole tile CSR (offsets,
+    ranks, tile keys) equal the oracle's prepare_scene / bin_tiles
+    (raster_forward.py:79-149) for C2, one C3 bench view and one C4 eye."""
+    from paper_2503_14171_b200.scenes import view_scene
+    c, sc, v = _scale_case(cfg)
+    P.render_forward(sc, c.width, c.height, view=v)   # sizes the pair capacity for this scene
+    pack = P.prepare_scene(sc, c.width, c.height, view=v)
+    _, bins = P.bin_tiles(pack, c.width, c.height)
+    osc = oracle.OScene.of(view_scene(sc, v) if v is not None else sc)
+    opack = oracle.prepare_scene(osc, c.width, c.height)
+    assert np.array_equal(pack.order.cpu().numpy(), opack.order)
+    bb, ob = pack.bboxes.cpu().numpy(), opack.bboxes
+    valid = pack.valid.cpu().numpy()
+    assert np.array_equal(valid, opack.valid), int((valid != opack.valid).sum())
+    # bboxes of valid splats are exact (an invalid splat's box is never used; the device
+    # stores it clipped to int16)
+    assert np.array_equal(bb[valid], ob[valid]), int((bb[valid] != ob[valid]).any(axis=1).sum())
+    off, ranks, keys = oracle.bin_tiles_csr(opack, c.width, c.height)
+    assert np.array_equal(bins.offsets.cpu().numpy(), off)
+    assert np.array_equal(bins.ranks.cpu().numpy(), ranks)
+    assert np.array_equal(bins.keys.cpu().numpy(), keys)
+
+
+def test_four_slot_pipeline_matches_oracle_c3(P, oracle):
+    """The bench's concurrent path at full C3 size: 8 views of the headline batch through
+    the 4-slot ViewPipeline (4 streams in flight) from a freshly uploaded DeviceScene
+    (non-blocking pinned upload + prepare, nothing synchronised before render) equal the
+    single-view API bitwise and the float64 oracle within 1e-4 / PSNR >= 60 dB."""
+    import torch
+    from paper_2503_14171_b200.device import FIELDS as SFIELDS, DeviceScene
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    from paper_2503_14171_b200.scenes import CONFIGS, random_views, synthetic_scene, view_scene
+    c = CONFIGS["c3"]
+    sc = synthetic_scene(c.n, c.width, c.height, c.scale_range, seed=5)
+    views = random_views(c.views, c.width, c.height, seed=11)[:8]
+    calib = ViewPipeline(sc, c.width, c.height, factor=c.factor, slots=1, views_for_capacity=views)
+    host = {f: torch.from_numpy(np.ascontiguousarray(getattr(sc, f))).pin_memory() for f in SFIELDS}
+    torch.cuda.synchronize()
+    ds = DeviceScene(**{k: t.to("cuda", non_blocking=True) for k, t in host.items()},
+                     background=tuple(sc.background), reference_resolution=tuple(sc.reference_resolution)).prepare()
+    pipe = ViewPipeline(ds, c.width, c.height, factor=c.factor, slots=4, capacity=calib.capacity)
+    out = torch.empty((len(views), c.out_h, c.out_w, 3), dtype=torch.float32, device="cuda")
+    pipe.render(views, out=out)
+    pipe.join()
+    torch.cuda.synchronize()
+    pipe.check()
+    for i, v in enumerate(views):
+        single = P.upscale_spline(P.render_forward(sc, c.width, c.height, view=v), c.factor)
+        assert torch.equal(out[i], single), i
+        ref = oracle.render_forward(view_scene(sc, v), c.width, c.height)
+        refup = oracle.upscale_spline(ref.color, ref.d_dx, ref.d_dy, ref.d_dxdy, c.factor)
+        diff = out[i].cpu().numpy() - refup
+        assert np.abs(diff).max() < PLANE_TOL, (i, np.abs(diff).max())
+        assert 10 * np.log10(1.0 / np.mean(diff ** 2)) >= 60.0
+
+
+def test_pipeline_rejects_bad_outputs(P):
+    import torch
+    from paper_2503_14171_b200.core import DimensionError
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    sc = P.synthetic_scene(2000, 64, 32, (0.5, 2.5), seed=1)
+    pipe = ViewPipeline(sc, 64, 32, factor=2.0, slots=2)
+    img = P.render_forward(sc, 64, 32)
+    for bad in (torch.empty((64, 128, 3), device="cuda", dtype=torch.float64),
+                torch.empty((64, 127, 3), device="cuda"),
+                torch.empty((64, 128, 4), device="cuda")[:, :, :3],
+                torch.empty(64 * 128 * 3 + 1, device="cuda")[1:].view(64, 128, 3),
+                torch.empty((64, 128, 3))):
+        with pytest.raises(DimensionError):
+            P.upscale_spline(img, 2.0, out=bad)
+        with pytest.raises(DimensionError):
+            pipe.render([None], out=bad[None])
+    ok = torch.empty((64, 128, 3), device="cuda")
+    assert torch.equal(P.upscale_spline(img, 2.0, out=ok), P.upscale_spline(img, 2.0))
