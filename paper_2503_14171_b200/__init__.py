@@ -8,7 +8,8 @@ hand-written sm_100a CUDA kernels in libsplat_b200.so behind a C ABI
 """
 
 from .core import (ALPHA_CLAMP, ALPHA_CULL, EARLY_TERMINATION, DegenerateCovarianceError,
-                   DimensionError, ParameterError, Scene, UnsupportedScaleError, logistic, logit)
+                   DimensionError, Gaussian2D, ParameterError, Scene, UnsupportedScaleError, logistic,
+                   logit)
 from .raster_forward import (GradientImage, RenderPack, bin_tiles, prepare_scene, render_at_points,
                              render_forward, sort_by_depth, tile_grid)
 from .raster_backward import (GradBuffer, PixelAdjoint, SceneGrads, invert_alpha_state,
@@ -21,7 +22,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "ALPHA_CLAMP", "ALPHA_CULL", "EARLY_TERMINATION", "DegenerateCovarianceError", "DimensionError",
-    "ParameterError", "Scene", "UnsupportedScaleError", "logistic", "logit", "GradientImage",
+    "ParameterError", "Scene", "Gaussian2D", "UnsupportedScaleError", "logistic", "logit", "GradientImage",
     "RenderPack", "bin_tiles", "prepare_scene", "render_at_points", "render_forward", "sort_by_depth",
     "tile_grid",
     "GradBuffer", "PixelAdjoint", "SceneGrads", "invert_alpha_state", "render_backward",

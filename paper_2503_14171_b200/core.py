@@ -48,6 +48,28 @@ def logit(p):
     return np.log(p) - np.log1p(-p)
 
 
+@dataclass(frozen=True)
+class Gaussian2D:
+    """One splat in reference-resolution pixels (core.py:53-72): a value object;
+    the renderer only ever sees the struct-of-arrays ``Scene``."""
+
+    mean: tuple
+    log_scale: tuple
+    rotation: float
+    opacity_logit: float
+    color: tuple
+    depth: float
+
+    def __post_init__(self):
+        flat = [*self.mean, *self.log_scale, self.rotation, self.opacity_logit, *self.color, self.depth]
+        if not np.all(np.isfinite(np.asarray(flat, dtype=np.float64))):
+            raise ParameterError("Gaussian2D requires finite parameters")
+
+    @property
+    def opacity(self) -> float:
+        return float(logistic(self.opacity_logit))
+
+
 @dataclass
 class Scene:
     """Splats over a reference-resolution canvas, struct-of-arrays float64.
@@ -84,6 +106,31 @@ class Scene:
     @property
     def n(self) -> int:
         return len(self.depths)
+
+    def gaussian(self, i: int) -> Gaussian2D:
+        """Splat ``i`` as a value object (core.py:117-125)."""
+        return Gaussian2D(mean=tuple(float(v) for v in self.means[i]),
+                          log_scale=tuple(float(v) for v in self.log_scales[i]),
+                          rotation=float(self.rotations[i]), opacity_logit=float(self.opacity_logits[i]),
+                          color=tuple(float(v) for v in self.colors[i]), depth=float(self.depths[i]))
+
+    @property
+    def gaussians(self) -> list:
+        """Every splat as a Gaussian2D, storage order (core.py:113-115)."""
+        return [self.gaussian(i) for i in range(self.n)]
+
+    @classmethod
+    def from_gaussians(cls, gaussians, background=(0.0, 0.0, 0.0), reference_resolution=(64, 64)) -> "Scene":
+        """Struct-of-arrays scene from value objects (core.py:127-143)."""
+        gs = list(gaussians)
+
+        def col(get, width):
+            a = np.asarray([get(g) for g in gs], dtype=np.float64)
+            return a.reshape(len(gs), width) if width > 1 else a.reshape(len(gs))
+
+        return cls(col(lambda g: g.mean, 2), col(lambda g: g.log_scale, 2), col(lambda g: g.rotation, 1),
+                   col(lambda g: g.opacity_logit, 1), col(lambda g: g.color, 3), col(lambda g: g.depth, 1),
+                   np.asarray(background, dtype=np.float64), reference_resolution)
 
     def touch(self) -> None:
         """Mark parameters as changed (invalidates the device copy)."""

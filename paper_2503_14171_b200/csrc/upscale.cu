@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(32 * UP_X4_WARPS, UP_X4_MINB) upscale_x4_kerne
 // output pixels); persistent, TMA-staged source double buffer, TMA bulk stores.
 constexpr int kX2Groups = 32;
 #ifndef UP_X2_WARPS
-#define UP_X2_WARPS 8
+#define UP_X2_WARPS 4
 #endif
 constexpr int kX2CellRows = UP_X2_WARPS;   // cell rows per tile = warps per CTA
 constexpr int kX2SpanC = 2 * kX2Groups + 2;   // corner columns 2 g0 - 1 .. 2 g0 + 64
