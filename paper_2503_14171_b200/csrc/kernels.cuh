@@ -19,11 +19,32 @@ int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, c
 // Frame workspace layout (all offsets 256-byte aligned).
 struct FrameLayout {
     size_t bboxes, touched, offsets, scan_scratch, keys0, vals0, vals1, slot_pos, tile_scan,
-        ranges, tile_count, tile_start, cursor, big_list, bin_hist, bin_part, counters, fixup, pack, total;
+        ranges, tile_count, tile_start, cursor, big_list, bin_hist, bin_part, counters, fixup, pack, rmask, total;
     int64_t n, cap;
     int width, height, ntx, nty;
 };
 FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap);
+
+// Tail padding of the per-pair arrays (ranks, rect masks): the rasterizer streams them
+// in 128-pair batches aligned down to 16 pairs, so a batch may read up to this many
+// entries past the last pair.
+constexpr int kPairPad = 160;
+
+// The rasterizer's 8x4-pixel rectangles of a 16x16 tile: rectangle (col, row), col 0..1,
+// row 0..3, is bit 2 row + col.  Bit set when the pair's bbox [x0, x1) x [y0, y1) overlaps
+// the rectangle's pixels: the reference tests each pixel against the bbox
+// (_kernels.py:61-64), so a rectangle whose bit is clear never sees the candidate.
+__device__ __forceinline__ uint32_t rect_mask(short4 bb, int tx, int ty) {
+    const int px0 = tx * kTile, py0 = ty * kTile;
+    uint32_t cols = 0, m = 0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+        if (bb.x < px0 + 8 * c + 8 && bb.y > px0 + 8 * c) cols |= 1u << c;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (bb.z < py0 + 4 * r + 4 && bb.w > py0 + 4 * r) m |= cols << (2 * r);
+    return m;
+}
 
 // Scene-constant layout inside const_buf.
 struct ConstLayout {

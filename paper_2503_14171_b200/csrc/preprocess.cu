@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ part, const uint32_t* __restrict__ tile_start,
     const uint32_t* __restrict__ tile_count, uint32_t* __restrict__ ranges, int64_t cap,
     uint32_t* __restrict__ ranks, uint32_t* __restrict__ keys, uint32_t* __restrict__ counters,
-    const uint32_t* __restrict__ offsets, uint32_t* __restrict__ slot_pos) {
+    const uint32_t* __restrict__ offsets, uint32_t* __restrict__ slot_pos, uint8_t* __restrict__ rmask) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ uint32_t wsum[33];
     __shared__ int pass_end;
@@ -464,18 +464,30 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
                 for (int j = a; j < e; ++j) below += stage[j] < v;
                 const uint32_t pos = gbase[t] + s0 + (uint32_t)a + below;
                 put_rank(pos, v, cap, ranks, counters);
-                if (keys && (int64_t)pos < cap) keys[pos] = (uint32_t)t;
-                if (slot_pos) {   // training: emission slot -> list position (see slot_map_kernel)
-                    const short4 b = bboxes[v];
-                    const int tx0 = b.x >> 4, ty0 = b.z >> 4, nx = ((b.y - 1) >> 4) - tx0 + 1;
-                    const int64_t e = (int64_t)offsets[v] + (t / ntx - ty0) * nx + (t % ntx - tx0);
-                    if (e < cap) slot_pos[e] = pos;
+                if ((int64_t)pos < cap) {
+                    if (keys) keys[pos] = (uint32_t)t;
+                    const short4 b = bboxes[v];   // the block's boxes: L1 / L2 hits
+                    rmask[pos] = (uint8_t)rect_mask(b, t % ntx, t / ntx);
+                    if (slot_pos) {   // training: emission slot -> list position (see slot_map_kernel)
+                        const int tx0 = b.x >> 4, ty0 = b.z >> 4, nx = ((b.y - 1) >> 4) - tx0 + 1;
+                        const int64_t e = (int64_t)offsets[v] + (t / ntx - ty0) * nx + (t % ntx - tx0);
+                        if (e < cap) slot_pos[e] = pos;
+                    }
                 }
             }
             __syncthreads();
             t0 = t1;
         }
     }
+}
+
+// Large-grid path: the per-pair rectangle masks once the lists are sorted.
+__global__ void rect_mask_kernel(int ntx, const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ ranks,
+                                 const short4* __restrict__ bboxes, uint8_t* __restrict__ rmask) {
+    const int t = blockIdx.x;
+    const uint32_t st = ranges[2 * t], en = ranges[2 * t + 1];
+    for (uint32_t j = st + threadIdx.x; j < en; j += blockDim.x)
+        rmask[j] = (uint8_t)rect_mask(bboxes[ranks[j]], t % ntx, t / ntx);
 }
 
 // Training mode: list position of every pair, indexed by its emission slot
@@ -698,7 +710,7 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap) {
     L.offsets = o; o = align_up(o + (nn + 1) * 4);
     L.scan_scratch = o; o = align_up(o + (size_t)scan_scratch_words(n + 1) * 4);
     L.keys0 = o; o = align_up(o + cc * 4);
-    L.vals0 = o; o = align_up(o + cc * 4);
+    L.vals0 = o; o = align_up(o + (cc + kPairPad) * 4);
     L.vals1 = o; o = align_up(o + cc * 4);   // merge buffer for very long tile lists
     L.slot_pos = o; o = align_up(o + cc * 4);   // training: list position of each emission slot
     L.tile_scan = o; o = align_up(o + (size_t)scan_scratch_words((int64_t)L.ntx * L.nty) * 4);
@@ -716,6 +728,7 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap) {
     L.counters = o; o = align_up(o + 16 * 4);
     L.fixup = o; o = align_up(o + (size_t)width * height * 4 + 4);
     L.pack = o; o = align_up(o + nn * sizeof(PackF));
+    L.rmask = o; o = align_up(o + cc + kPairPad);   // per pair: rect_mask of its tile (u8)
     L.total = o;
     return L;
 }
@@ -858,7 +871,8 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         fill_rows_kernel<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, part,
                                                                   tile_start, tile_count, ranges, L.cap, ranks,
                                                                   keys, counters, (const uint32_t*)(ws + L.offsets),
-                                                                  with_offsets ? (uint32_t*)(ws + L.slot_pos) : nullptr);
+                                                                  with_offsets ? (uint32_t*)(ws + L.slot_pos) : nullptr,
+                                                                  (uint8_t*)(ws + L.rmask));
         note_launch();
         SPLAT_CUDA_CHECK(cudaGetLastError());
         return SPLAT_OK;
@@ -887,6 +901,8 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
     note_launch();
     segsort_large_kernel<<<148, kSegThreadsLarge, kSegChunk * 4, stream>>>(ranges, ranks, (uint32_t*)(ws + L.vals1),
                                                                           keys, big, counters);
+    note_launch();
+    rect_mask_kernel<<<ntiles, 256, 0, stream>>>(L.ntx, ranges, ranks, bboxes, (uint8_t*)(ws + L.rmask));
     note_launch();
     if (with_offsets) {
         slot_map_kernel<<<ntiles, 256, 0, stream>>>(L.ntx, ranges, ranks, bboxes, (const uint32_t*)(ws + L.offsets),

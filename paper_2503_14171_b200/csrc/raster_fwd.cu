@@ -32,6 +32,7 @@ struct RasterArgs {
     int width, height, ntx;
     const uint32_t* ranges;
     const uint32_t* ranks;
+    const uint8_t* rmask;
     const PackF* pack;
     const short4* bboxes;
     float* planes;
@@ -330,10 +331,36 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// Pair batches: the tile list (ranks + per-pair rectangle masks, written by the
+// binning) is read 128 pairs at a time with TMA bulk copies (cp.async.bulk ->
+// UBLKCP, completion on a per-warp mbarrier), aligned down to 16 pairs.
+constexpr int kBatch = 128;
+constexpr int kQueue = 256;   // compaction ring: < 32 queued + one batch always fit
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
 template <bool TRAIN>
 __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_kernel(RasterArgs p) {
     // per warp, double-buffered: chunk c+1 is fetched with cp.async (LDGSTS) while chunk c blends
-#if RASTER_PACK_PAD
     // 80-byte stride: the four groups' candidates of a step fall on different banks
     struct PackS {
         PackF f;
@@ -342,17 +369,25 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
     __shared__ PackS s_packs[kWarps][2][32];
 #define S_PACK(w, b, i) (s_packs[w][b][i].f)
 #define S_COL(w, b, i) (s_packs[w][b][i].col)
-#else
-    __shared__ PackF s_pack[kWarps][2][32];
-    __shared__ float4 s_col[kWarps][2][32];
-#define S_PACK(w, b, i) (s_pack[w][b][i])
-#define S_COL(w, b, i) (s_col[w][b][i])
-#endif
     __shared__ uint32_t s_rank[kWarps][2][32];
+    __shared__ uint32_t s_pos[kWarps][TRAIN ? 2 : 1][32];                 // list positions (training)
+    __shared__ __align__(16) uint32_t s_braw[kWarps][2][kBatch];          // batch: ranks
+    __shared__ __align__(16) uint32_t s_bmask[kWarps][2][kBatch / 4];     // batch: rect masks (u8 x 4)
+    __shared__ uint32_t s_qr[kWarps][kQueue];                             // queue: ranks
+    __shared__ uint32_t s_qp[kWarps][TRAIN ? kQueue : 1];                 // queue: list positions
+    __shared__ __align__(8) uint64_t s_bbar[kWarps][2];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = lane >> 3, li = lane & 7;
     const uint32_t nunits = (uint32_t)(p.ntx * ((p.height + kTile - 1) / kTile)) * kRects;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_addr(&s_bbar[warp][0])));
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_addr(&s_bbar[warp][1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint32_t bphase = 0u;   // parity of the next completion of batch buffer k (bit k)
 
     // Persistent, per-warp dynamic scheduling: a warp claims (tile, 8x4 rectangle)
     // units from a global counter, so neither slow warps of a CTA nor the last wave
@@ -378,83 +413,108 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
         bool active = inside;
         bool flagged = false;
 
-        // lane copies its candidate of the chunk at cbase into buffer b
-        auto stage = [&](uint32_t cbase, int b, uint32_t r) {
-            if (cbase + lane < end) {
-                const float4* src = reinterpret_cast<const float4*>(p.pack + r);
-                float4* dst = reinterpret_cast<float4*>(&S_PACK(warp, b, lane));
-                cp_async16(dst, src);
-                cp_async16(dst + 1, src + 1);
-                cp_async16(dst + 2, src + 2);
-                cp_async16(dst + 3, src + 3);
-                cp_async16(&S_COL(warp, b, lane), p.sc.color + r);
-                s_rank[warp][b][lane] = r;
-            }
-            cp_async_commit();
-        };
-
         if (__any_sync(0xffffffffu, active) && start < end) {
-            stage(start, 0, start + lane < end ? p.ranks[start + lane] : 0u);
-            uint32_t r_next = start + 32 + lane < end ? p.ranks[start + 32 + lane] : 0u;
-            int b = 0;
-            for (uint32_t base = start; base < end; base += 32, b ^= 1) {
-                if (base + 32 < end) {
-                    stage(base + 32, b ^ 1, r_next);
-                    r_next = base + 64 + lane < end ? p.ranks[base + 64 + lane] : 0u;
-                } else {
-                    cp_async_commit();   // one group per chunk: wait_group 1 == "chunk base landed"
+            // The tile list is compacted to the pairs whose bbox reaches this warp's
+            // rectangle (binning's rect masks, ~40% of the list at C3) before any
+            // candidate is staged: batches of 128 pairs land in shared memory by bulk
+            // copy, a ballot scan appends the kept (rank, position) pairs in list order to
+            // a per-warp ring, and chunks of 32 kept candidates are staged from the ring.
+            const uint32_t b0 = start & ~15u;
+            auto issue_batch = [&](uint32_t bstart, int k) {   // lane 0
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(&s_bbar[warp][k])),
+                             "r"((uint32_t)(kBatch * 4 + kBatch)) : "memory");
+                bulk_g2s(&s_braw[warp][k][0], p.ranks + bstart, kBatch * 4, &s_bbar[warp][k]);
+                bulk_g2s(&s_bmask[warp][k][0], p.rmask + bstart, kBatch, &s_bbar[warp][k]);
+            };
+            if (lane == 0) {
+                issue_batch(b0, 0);
+                if (b0 + kBatch < end) issue_batch(b0 + kBatch, 1);
+            }
+            uint32_t bnext = b0;         // first pair of the next batch to scan
+            uint32_t qh = 0, qt = 0;     // ring head (next to stage) / tail (next free)
+            // scan batches until 32 candidates are queued or the list is exhausted
+            auto refill = [&]() {
+                while (qt - qh < 32u && bnext < end) {
+                    const int k = (int)((bnext - b0) / kBatch) & 1;
+                    mbar_wait_parity(&s_bbar[warp][k], (bphase >> k) & 1u);
+                    bphase ^= 1u << k;
+                    const uint32_t m4 = s_bmask[warp][k][lane];
+                    const uint32_t pos0 = bnext + 4u * (uint32_t)lane;
+                    uint32_t keep = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t pos = pos0 + (uint32_t)j;
+                        if (((m4 >> (8 * j + wr)) & 1u) && pos >= start && pos < end) keep |= 1u << j;
+                    }
+                    const uint32_t c = __popc(keep);
+                    const uint32_t v0 = __ballot_sync(0xffffffffu, c & 1u), v1 = __ballot_sync(0xffffffffu, c & 2u),
+                                   v2 = __ballot_sync(0xffffffffu, c & 4u);
+                    uint32_t at = qt + __popc(v0 & lt_mask) + 2u * __popc(v1 & lt_mask) + 4u * __popc(v2 & lt_mask);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if ((keep >> j) & 1u) {
+                            s_qr[warp][at & (kQueue - 1)] = s_braw[warp][k][4 * lane + j];
+                            if (TRAIN) s_qp[warp][at & (kQueue - 1)] = pos0 + (uint32_t)j;
+                            ++at;
+                        }
+                    qt += __popc(v0) + 2u * __popc(v1) + 4u * __popc(v2);
+                    __syncwarp();   // the batch buffer is read: it may be refilled
+                    bnext += kBatch;
+                    if (lane == 0 && bnext + kBatch < end) issue_batch(bnext + kBatch, k);
                 }
-                cp_async_wait1();
+                __syncwarp();
+            };
+            // lane copies queued candidate qh + lane into chunk buffer b; returns the chunk size
+            auto stage = [&](int b) -> int {
+                const int n = (int)min(32u, qt - qh);
+                if (lane < n) {
+                    const uint32_t e = (qh + (uint32_t)lane) & (kQueue - 1);
+                    const uint32_t r = s_qr[warp][e];
+                    const float4* src = reinterpret_cast<const float4*>(p.pack + r);
+                    float4* dst = reinterpret_cast<float4*>(&S_PACK(warp, b, lane));
+                    cp_async16(dst, src);
+                    cp_async16(dst + 1, src + 1);
+                    cp_async16(dst + 2, src + 2);
+                    cp_async16(dst + 3, src + 3);
+                    cp_async16(&S_COL(warp, b, lane), p.sc.color + r);
+                    s_rank[warp][b][lane] = r;
+                    if (TRAIN) s_pos[warp][TRAIN ? b : 0][lane] = s_qp[warp][TRAIN ? e : 0];
+                }
+                cp_async_commit();   // one group per chunk (possibly empty)
+                qh += (uint32_t)n;
+                return n;
+            };
+            refill();
+            int ncur = stage(0);
+            int b = 0;
+            while (ncur > 0) {
+                refill();
+                const int nnext = stage(b ^ 1);
+                cp_async_wait1();   // chunk b landed (the next one may still be in flight)
                 __syncwarp();
                 uint32_t gmask = 0;   // bit g: candidate reaches group g's 4x2 rectangle
-                if (base + lane < end) {
+                if (lane < ncur) {
                     const PackF g = S_PACK(warp, b, lane);
-                    if (RASTER_NO_WARP_EXACT || ellipse_hits_rect(g, X0, X0 + 7.f, Y0, Y0 + 3.f)) {
-#if RASTER_GROUP_EXACT
-                        // groups: the exact ellipse test against each 4x2 rectangle
-                        gmask = (ellipse_hits_rect(g, X0, X0 + 3.f, Y0, Y0 + 1.f) ? 1u : 0u) |
-                                (ellipse_hits_rect(g, X0 + 4.f, X0 + 7.f, Y0, Y0 + 1.f) ? 2u : 0u) |
-                                (ellipse_hits_rect(g, X0, X0 + 3.f, Y0 + 2.f, Y0 + 3.f) ? 4u : 0u) |
-                                (ellipse_hits_rect(g, X0 + 4.f, X0 + 7.f, Y0 + 2.f, Y0 + 3.f) ? 8u : 0u);
-#else
-                        // groups: the cull ellipse's extent box against each 4x2 rectangle
-                        const float lx = g.mxh - g.ex, hx = g.mxh + g.ex;
-                        const float ly = g.myh - g.ey, hy = g.myh + g.ey;
-                        const uint32_t c0 = (lx <= X0 + 3.f && hx >= X0) ? 1u : 0u;
-                        const uint32_t c1 = (lx <= X0 + 7.f && hx >= X0 + 4.f) ? 1u : 0u;
-                        const uint32_t r0 = (ly <= Y0 + 1.f && hy >= Y0) ? 1u : 0u;
-                        const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
-                        gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
-#if RASTER_GROUP_DIL
-                        if (gmask) gmask &= group_qnorm_mask(g, X0, Y0);
-#endif
-#endif
-                    }
+                    // groups: the cull ellipse's extent box against each 4x2 rectangle
+                    const float lx = g.mxh - g.ex, hx = g.mxh + g.ex;
+                    const float ly = g.myh - g.ey, hy = g.myh + g.ey;
+                    const uint32_t c0 = (lx <= X0 + 3.f && hx >= X0) ? 1u : 0u;
+                    const uint32_t c1 = (lx <= X0 + 7.f && hx >= X0 + 4.f) ? 1u : 0u;
+                    const uint32_t r0 = (ly <= Y0 + 1.f && hy >= Y0) ? 1u : 0u;
+                    const uint32_t r1 = (ly <= Y0 + 3.f && hy >= Y0 + 2.f) ? 1u : 0u;
+                    gmask = (c0 & r0) | ((c1 & r0) << 1) | ((c0 & r1) << 2) | ((c1 & r1) << 3);
+                    if (gmask) gmask &= group_qnorm_mask(g, X0, Y0);
                 }
                 int cnt_max = 0;
                 uint32_t my_mask = 0;   // this lane's group: candidates of the chunk, walked low to high
-#if RASTER_STATS
-                int cnt_sum = 0;
-#endif
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
                     const uint32_t mq = __ballot_sync(0xffffffffu, (gmask >> qq) & 1u);
-                    const int c = __popc(mq);
-                    cnt_max = max(cnt_max, c);
+                    cnt_max = max(cnt_max, __popc(mq));
                     if (qq == q) my_mask = mq;
-#if RASTER_STATS
-                    cnt_sum += c;
-#endif
                 }
-#if RASTER_STATS
-                if (lane == 0) {
-                    atomicAdd((unsigned long long*)&p.counters[8], 1ull);
-                    atomicAdd((unsigned long long*)&p.counters[10], (unsigned long long)cnt_max);
-                    atomicAdd((unsigned long long*)&p.counters[12], (unsigned long long)cnt_sum);
-                }
-#endif
                 __syncwarp();
-#if RASTER_UNROLL > 1 && !RASTER_STATS
                 // RASTER_UNROLL steps per iteration in inference (a step with an empty list is a
                 // no-op, so the tail needs no guard): less loop-back and termination-vote
                 // overhead.  Training keeps one step (its float64 state has no registers to spare).
@@ -466,34 +526,26 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                             const int idx = __ffs(my_mask) - 1;
                             my_mask &= my_mask - 1u;
                             blend_candidate<TRAIN>(p, S_PACK(warp, b, idx), S_COL(warp, b, idx),
-                                                   &s_rank[warp][b][idx], base + idx, cx, cy, s, active,
-                                                   flagged);
+                                                   &s_rank[warp][b][idx], TRAIN ? s_pos[warp][TRAIN ? b : 0][idx] : 0u,
+                                                   cx, cy, s, active, flagged);
                         }
                     }
                     if (((k + kU) & 7) == 0 && !__any_sync(0xffffffffu, active)) break;
                 }
-#else
-                for (int k = 0; k < cnt_max; ++k) {
-#if RASTER_STATS
-                    {
-                        const uint32_t ev = __ballot_sync(0xffffffffu, active && my_mask != 0u);
-                        if (lane == 0) atomicAdd((unsigned long long*)&p.counters[14], (unsigned long long)__popc(ev));
-                    }
-#endif
-                    if (active && my_mask != 0u) {
-                        const int idx = __ffs(my_mask) - 1;
-                        my_mask &= my_mask - 1u;
-                        blend_candidate<TRAIN>(p, S_PACK(warp, b, idx), S_COL(warp, b, idx),
-                                               &s_rank[warp][b][idx], base + idx, cx, cy, s, active,
-                                               flagged);
-                    }
-                    if ((k & RASTER_TERM_MASK) == RASTER_TERM_MASK && !__any_sync(0xffffffffu, active)) break;
-                }
-#endif
                 if (!__any_sync(0xffffffffu, active)) break;
                 __syncwarp();
+                ncur = nnext;
+                b ^= 1;
             }
             cp_async_wait0();
+            // batches still in flight must land before their buffers and barriers are reused
+            // (the batches in flight are always those at bnext and bnext + kBatch below end)
+            for (int i = 0; i < 2 && bnext < end; ++i) {
+                const int k = (int)((bnext - b0) / kBatch) & 1;
+                mbar_wait_parity(&s_bbar[warp][k], (bphase >> k) & 1u);
+                bphase ^= 1u << k;
+                bnext += kBatch;
+            }
             __syncwarp();
         }
         if (inside) {
@@ -673,6 +725,7 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
     a.ntx = L.ntx;
     a.ranges = (const uint32_t*)(ws + L.ranges);
     a.ranks = (const uint32_t*)(ws + L.vals0);
+    a.rmask = (const uint8_t*)(ws + L.rmask);
     a.pack = (const PackF*)(ws + L.pack);
     a.bboxes = (const short4*)(ws + L.bboxes);
     a.planes = out.planes;
