@@ -201,8 +201,20 @@ class ViewTrainer:
             img = render_forward(self.ds, rw, rh, view=v, train=True)
             need = max(need, img.stats.get("pairs", 0))
         key = (self.ds.n, rw, rh)
-        _capacity_hint[key] = max(_initial_capacity(self.ds.n, rw, rh), int(need * 1.5) + 4096)
-        self._frames = []
+        cap = max(_initial_capacity(self.ds.n, rw, rh), int(need * 1.5) + 4096)
+        _capacity_hint[key] = cap
+        # per-stream steady-state buffers, reused by every view of that stream in every
+        # step (stream order makes the reuse safe): the training image, its bin
+        # workspace, the upscaled prediction, the source adjoint, the backward workspace
+        from .raster_forward import Frame, GradientImage
+        w, h = self.out_size
+        dev, lib = self.ds.device, _lib.load()
+        self._imgs = [GradientImage.empty(rw, rh, dev, train=True) for _ in range(self.streams)]
+        self._frames = [Frame(self.ds.n, rw, rh, cap, dev) for _ in range(self.streams)]
+        self._preds = [torch.empty((h, w, 3), dtype=torch.float32, device=dev) for _ in range(self.streams)]
+        self._sadjs = [torch.empty((rh, rw, 4, 3), dtype=torch.float32, device=dev) for _ in range(self.streams)]
+        nb = lib.splat_backward_workspace_bytes(self.ds.n, cap)
+        self._bws = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(self.streams)]
 
     def check(self) -> None:
         """Synchronise and raise if any frame of the last step overflowed its pair buffer."""
@@ -229,24 +241,24 @@ class ViewTrainer:
             self._spare_free.record(main)
         for st in self._streams:
             st.wait_stream(main)
-        self._frames = []
         for i, (v, tgt) in enumerate(zip(self.views, self.targets)):
             k = i % self.streams
             with torch.cuda.stream(self._streams[k]):
                 adj_img = self._adjs[k]
-                fwd = render_forward(ds, rw, rh, view=v, train=True, sync_check=False)
-                self._frames.append(fwd.frame)
+                fwd = render_forward(ds, rw, rh, view=v, train=True, sync_check=False, out=self._imgs[k],
+                                     frame=self._frames[k])
                 # fit.py:192-212: the analytic channels, or classical bicubic from FD planes
                 src = fwd if self.upscale_mode == "spline_analytic" else fd_gradients(fwd.color)
-                pred = upscale_spline(src, 1.0, out_size=(w, h))
+                pred = upscale_spline(src, 1.0, out_size=(w, h), out=self._preds[k])
                 loss_device(pred, tgt, self.ssim_weight, adj=adj_img, value=self.values[i], slot=k)
-                sadj = upscale_backward(src, 1.0, adj_img, out_size=(w, h))
+                sadj = upscale_backward(src, 1.0, adj_img, out_size=(w, h), out=self._sadjs[k])
                 if self.upscale_mode == "spline_analytic":
                     adj = PixelAdjoint.from_source(sadj)
                 else:
                     adj = PixelAdjoint.zeros(rw, rh, ds.device)
                     adj.planes[:, :, 0, :] = fd_gradients_backward(sadj)
-                render_backward_rank(ds, fwd, adj, self._slot_rank[k], accumulate=i >= self.streams)
+                render_backward_rank(ds, fwd, adj, self._slot_rank[k], accumulate=i >= self.streams,
+                                     workspace=self._bws[k])
         for st in self._streams:
             main.wait_stream(st)
         lib = _lib.load()

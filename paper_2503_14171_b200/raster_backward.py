@@ -21,7 +21,7 @@ import torch
 
 from . import _lib
 from .core import DimensionError, ParameterError
-from .device import to_device
+from .device import DeviceScene, to_device
 from .raster_forward import GradientImage, make_view, render_forward
 
 __all__ = ["PixelAdjoint", "SceneGrads", "invert_alpha_state", "render_backward", "GradBuffer"]
@@ -162,7 +162,7 @@ def render_backward(scene, fwd: GradientImage, adj, *, threads: int = 1, view=No
 
 
 def render_backward_rank(ds: DeviceScene, fwd: GradientImage, adj, rank_grads: torch.Tensor,
-                         accumulate: bool = True) -> torch.Tensor:
+                         accumulate: bool = True, workspace: torch.Tensor | None = None) -> torch.Tensor:
     """Multi-view training building block: add this view's render-space gradient
     terms, view-scaled and in rank order ((n, 9) float32), into ``rank_grads``;
     :func:`chain_grads` maps the sum over views to parameter gradients once
@@ -176,7 +176,10 @@ def render_backward_rank(ds: DeviceScene, fwd: GradientImage, adj, rank_grads: t
     lib = _lib.load()
     frame = fwd.frame
     nbytes = lib.splat_backward_workspace_bytes(ds.n, frame.capacity)
-    bws = torch.empty(nbytes, dtype=torch.uint8, device=ds.device)
+    if workspace is not None and workspace.numel() >= nbytes:
+        bws = workspace
+    else:
+        bws = torch.empty(nbytes, dtype=torch.uint8, device=ds.device)
     _lib.check(lib.splat_render_backward_rank(_lib.ptr(ds.const), ds.c_scene(), fwd.view, w, h, fwd.c_gimg(),
                                               _lib.ptr(pa.planes), _lib.ptr(frame.ws), frame.nbytes,
                                               frame.capacity, _lib.ptr(bws), nbytes, _lib.ptr(rank_grads),

@@ -280,8 +280,11 @@ def bin_tiles(pack: RenderPack, out_w: int, out_h: int, *, _flags: int = 0):
 
 def render_forward(scene, out_width: int, out_height: int, *, tiled: bool = True, threads: int = 1,
                    view=None, train: bool = False, out: GradientImage | None = None,
-                   sync_check: bool = True) -> GradientImage:
-    """Render with analytic gradients (raster_forward.py:152-187)."""
+                   sync_check: bool = True, frame: "Frame | None" = None) -> GradientImage:
+    """Render with analytic gradients (raster_forward.py:152-187).
+
+    ``out`` / ``frame`` reuse a caller's image and bin workspace (steady-state loops);
+    a reused frame keeps its capacity, and an overflow stays flagged in its counters."""
     del tiled, threads  # output-invariant by the reference's contract
     if out_width <= 0 or out_height <= 0:
         raise DimensionError("output dimensions must be positive")
@@ -293,9 +296,12 @@ def render_forward(scene, out_width: int, out_height: int, *, tiled: bool = True
     v = make_view(ds, out_width, out_height, view)
     img.scene, img.view = ds, v
     st = _lib.stream_ptr()
-    cap = _initial_capacity(ds.n, out_width, out_height)
+    if frame is not None and (frame.n, frame.width, frame.height) != (ds.n, out_width, out_height):
+        raise DimensionError("frame workspace was sized for another scene or resolution")
+    cap = frame.capacity if frame is not None else _initial_capacity(ds.n, out_width, out_height)
     while True:
-        frame = Frame(ds.n, out_width, out_height, cap, ds.device)
+        if frame is None or frame.capacity < cap:
+            frame = Frame(ds.n, out_width, out_height, cap, ds.device)
         _lib.check(lib.splat_render_forward(_lib.ptr(ds.const), ds.n, v, out_width, out_height,
                                             int(train), img.c_gimg(), _lib.ptr(frame.ws), frame.nbytes,
                                             frame.capacity, st))

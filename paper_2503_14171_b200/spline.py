@@ -118,7 +118,8 @@ class SourceAdjoint:
     d_dxdy = property(lambda s: s.planes[:, :, 3, :])
 
 
-def upscale_backward(img, factor: float, adjoint, *, out_size=None) -> SourceAdjoint:
+def upscale_backward(img, factor: float, adjoint, *, out_size=None,
+                     out: torch.Tensor | None = None) -> SourceAdjoint:
     """Exact transpose of the linear upscale map, clamp excluded (spline.py:191-229).
 
     Gather form: every source pixel's 12 adjoints are written once, in a fixed
@@ -135,7 +136,13 @@ def upscale_backward(img, factor: float, adjoint, *, out_size=None) -> SourceAdj
     if tuple(adj.shape) != (out_h, out_w, 3):
         raise DimensionError("adjoint dimensions must match the upscaled output")
     lib = _lib.load()
-    dsrc = torch.empty((h, w, 4, 3), dtype=torch.float32, device=dev)
+    if out is None:
+        dsrc = torch.empty((h, w, 4, 3), dtype=torch.float32, device=dev)
+    else:
+        if tuple(out.shape) != (h, w, 4, 3) or out.dtype != torch.float32 or not out.is_contiguous() \
+                or out.device != dev or out.data_ptr() % 16:
+            raise DimensionError("out must be a contiguous 16-byte aligned (H, W, 4, 3) float32 tensor")
+        dsrc = out
     _lib.check(lib.splat_upscale_backward(_lib.ptr(adj), out_w, out_h, _lib.ptr(dsrc), w, h,
                                           _lib.stream_ptr()))
     return SourceAdjoint(dsrc)
