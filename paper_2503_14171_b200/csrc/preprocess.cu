@@ -263,20 +263,23 @@ __global__ void __launch_bounds__(kBinThreads) count_rows_kernel(int64_t n, cons
     }
 }
 
-// Per (group, tile): exclusive prefix within the group's rows (in place) and the group sum.
-__global__ void colscan_rows_kernel(int ntiles, int nrows, uint32_t* __restrict__ hist, uint32_t* __restrict__ part) {
+// Per (group, tile): exclusive prefix within the group's rows (into pre; hist keeps the
+// counts, which the fill uses as its block's histogram) and the group sum.
+__global__ void colscan_rows_kernel(int ntiles, int nrows, const uint32_t* __restrict__ hist,
+                                    uint32_t* __restrict__ pre, uint32_t* __restrict__ part) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int g = blockIdx.y;
     if (t >= ntiles) return;
     const int r0 = g * kColGroup, nr = min(kColGroup, nrows - r0);
-    uint32_t* col = hist + (size_t)r0 * ntiles + t;
+    const uint32_t* col = hist + (size_t)r0 * ntiles + t;
+    uint32_t* out = pre + (size_t)r0 * ntiles + t;
     uint32_t v[kColGroup];
 #pragma unroll
     for (int i = 0; i < kColGroup; ++i) v[i] = i < nr ? col[(size_t)i * ntiles] : 0u;   // all loads in flight
     uint32_t run = 0;
 #pragma unroll
     for (int i = 0; i < kColGroup; ++i) {
-        if (i < nr) col[(size_t)i * ntiles] = run;
+        if (i < nr) out[(size_t)i * ntiles] = run;
         run += v[i];
     }
     part[(size_t)g * ntiles + t] = run;
@@ -384,7 +387,8 @@ __global__ void __launch_bounds__(1024) colscan_groups_scan_kernel(int ntiles, i
 
 __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
     int64_t n, const short4* __restrict__ bboxes, const uint32_t* __restrict__ touched, int ntx, int ntiles,
-    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ part, const uint32_t* __restrict__ tile_start,
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ pre, const uint32_t* __restrict__ part,
+    const uint32_t* __restrict__ tile_start,
     const uint32_t* __restrict__ tile_count, uint32_t* __restrict__ ranges, int64_t cap,
     uint32_t* __restrict__ ranks, uint32_t* __restrict__ keys, uint32_t* __restrict__ counters,
     const uint32_t* __restrict__ offsets, uint32_t* __restrict__ slot_pos, uint8_t* __restrict__ rmask) {
@@ -403,14 +407,11 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
 #pragma unroll
         for (int j = 0; j < kBinRPT; ++j)
             bb[j] = bin_box(n, blk * kBinBlock + j * kBinThreads + threadIdx.x, bboxes, touched);
-        for (int t = threadIdx.x; t < ntiles; t += blockDim.x) loff[t] = 0;
+        // this block's tile histogram is count_rows' row (no second counting pass)
+        const uint32_t* crow = hist + (size_t)blk * ntiles;
+        for (int t = threadIdx.x; t < ntiles; t += blockDim.x) loff[t] = crow[t];
         __syncthreads();
-#pragma unroll
-        for (int j = 0; j < kBinRPT; ++j)
-            for (int ty = bb[j].z >> 4; ty <= (bb[j].w - 1) >> 4; ++ty)
-                for (int tx = bb[j].x >> 4; tx <= (bb[j].y - 1) >> 4; ++tx) atomicAdd(&loff[ty * ntx + tx], 1u);
-        __syncthreads();
-        const uint32_t* hrow = hist + (size_t)blk * ntiles;
+        const uint32_t* hrow = pre + (size_t)blk * ntiles;
         const uint32_t* prow = part + (size_t)(blk / kColGroup) * ntiles;
         const uint32_t total = block_exclusive_scan(loff, ntiles, wsum);
         for (int t = threadIdx.x; t < ntiles; t += blockDim.x) gbase[t] = tile_start[t] + prow[t] + hrow[t] - loff[t];
@@ -722,6 +723,7 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap) {
         const size_t rows = (size_t)(nn + kBinBlock - 1) / kBinBlock;
         const size_t groups = (rows + kColGroup - 1) / kColGroup;
         L.bin_hist = o; o = align_up(o + rows * L.ntx * L.nty * 4);
+        L.bin_pre = o; o = align_up(o + rows * L.ntx * L.nty * 4);
         L.bin_part = o; o = align_up(o + groups * L.ntx * L.nty * 4);
     }
     L.big_list = o; o = align_up(o + (size_t)L.ntx * L.nty * 4);
@@ -851,12 +853,13 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         });
         if (rc != SPLAT_OK) return rc;
         uint32_t* hist = (uint32_t*)(ws + L.bin_hist);
+        uint32_t* pre = (uint32_t*)(ws + L.bin_pre);
         uint32_t* part = (uint32_t*)(ws + L.bin_part);
         const int grid = (int)(nrows < 148 * 2 ? nrows : 148 * 2);
         count_rows_kernel<<<grid, kBinThreads, ntiles * 4, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist);
         note_launch();
         colscan_rows_kernel<<<dim3(ceil_div(ntiles, 128), ngroups), 128, 0, stream>>>(ntiles, (int)nrows, hist,
-                                                                                     part);
+                                                                                     pre, part);
         note_launch();
         if (ntiles <= kScanTilesMax) {
             colscan_groups_scan_kernel<<<1, 1024, ntiles * 4, stream>>>(ntiles, ngroups, part, tile_count,
@@ -868,7 +871,7 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
             note_launch();
             exclusive_scan_u32(tile_count, tile_start, ntiles, scan_tmp, &counters[0], stream);
         }
-        fill_rows_kernel<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, part,
+        fill_rows_kernel<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, pre, part,
                                                                   tile_start, tile_count, ranges, L.cap, ranks,
                                                                   keys, counters, (const uint32_t*)(ws + L.offsets),
                                                                   with_offsets ? (uint32_t*)(ws + L.slot_pos) : nullptr,
