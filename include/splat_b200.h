@@ -98,6 +98,8 @@ const char *splat_last_error(void);
 int splat_abi_version(void);
 /* Number of kernels this library has launched since load (all streams). */
 uint64_t splat_kernel_launches(void);
+/* 1 for the checked build (device-side SPLAT_DCHECK bounds / protocol checks, `make checked`), else 0. */
+int splat_build_checked(void);
 
 /* ---- per-scene preparation (view independent) --------------------------
  * Stable depth argsort (raster_forward.py:59-61) and the view-independent

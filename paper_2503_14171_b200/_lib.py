@@ -56,6 +56,7 @@ SIGNATURES = {
     "splat_last_error": (ctypes.c_char_p, []),
     "splat_abi_version": (I32, []),
     "splat_kernel_launches": (ctypes.c_uint64, []),
+    "splat_build_checked": (I32, []),
     "splat_scene_const_bytes": (SZ, [I64]),
     "splat_scene_workspace_bytes": (SZ, [I64]),
     "splat_scene_prepare": (I32, [ctypes.POINTER(SceneT), P, SZ, P, SZ, P]),

@@ -85,6 +85,7 @@ extern "C" {
 const char* splat_last_error(void) { return g_err; }
 int splat_abi_version(void) { return SPLAT_ABI_VERSION; }
 uint64_t splat_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+int splat_build_checked(void) { return SPLAT_CHECKS; }
 
 size_t splat_scene_const_bytes(int64_t n) { return const_layout(n).total; }
 size_t splat_scene_workspace_bytes(int64_t n) { return scene_workspace_bytes_impl(n); }

@@ -2,6 +2,7 @@
 #pragma once
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <mutex>
 #include <cuda_runtime.h>
 
@@ -45,6 +46,29 @@ struct __align__(16) PackF {
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Device-side invariant checks of the checked build (`make checked` ->
+// libsplat_b200_checked.so): index and protocol bounds of the shared-memory rings,
+// staging buffers and scattered stores.  A violated check prints and traps, so the
+// launch fails loudly; the default build compiles them out.  (compute-sanitizer is
+// not available on this pool: this build plus the guard-band tests stand in for it.)
+#ifndef SPLAT_CHECKS
+#define SPLAT_CHECKS 0
+#endif
+#if SPLAT_CHECKS
+#define SPLAT_DCHECK(cond)                                                                          \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("SPLAT_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                             \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define SPLAT_DCHECK(cond) \
+    do {                   \
+    } while (0)
+#endif
 
 }  // namespace splat
 

@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
                         const int t = row + tx;
                         if (t < t0 || t >= t1) continue;
                         const uint32_t idx = atomicAdd(&loff[t], 1u) - s0;
+                        SPLAT_DCHECK(idx < (uint32_t)kBinStage);
                         stage[idx] = r;
                         stile[idx] = (uint16_t)t;
                     }
@@ -462,6 +463,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
                 const int a = t == t0 ? 0 : (int)(loff[t - 1] - s0);
                 const int e = (int)(loff[t] - s0);
                 uint32_t below = 0;
+                SPLAT_DCHECK(a <= i && i < e && e <= m);
                 for (int j = a; j < e; ++j) below += stage[j] < v;
                 const uint32_t pos = gbase[t] + s0 + (uint32_t)a + below;
                 put_rank(pos, v, cap, ranks, counters);

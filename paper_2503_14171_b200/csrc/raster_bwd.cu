@@ -189,7 +189,9 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
         // (skipped when none of its live pixels reaches back this far)
         const bool work = lo < warp_hi;
         bool keep = false;
+        SPLAT_DCHECK(nb >= 1 && nb <= kBwBatch);
         if (lane < nb) {
+            SPLAT_DCHECK((int64_t)r < p.sc.n);
             s_rank[warp][lane] = r;
             if (work) {
                 const PackF g = p.pack[r];
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
             prev = atomicAdd(&S.done[slot], 1);
         }
         prev = __shfl_sync(0xffffffffu, prev, 0);
+        SPLAT_DCHECK(prev >= 0 && prev < kWarps_bw);
         if (prev == kWarps_bw - 1) {
             __threadfence_block();
             // fixed warp order: one partial per (splat, tile) pair, at its list position
@@ -396,6 +399,7 @@ __global__ void __launch_bounds__(kBlock, 2) raster_bwd_kernel(BwdArgs p) {
                     }
                 }
                 {
+                    SPLAT_DCHECK(lo + lane >= start && lo + lane < end);
                     float* dst = p.partial + (size_t)(lo + lane) * kG;
 #pragma unroll
                     for (int i = 0; i < kG; ++i) dst[i] = acc[i];

@@ -406,6 +406,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
         const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
         const float X0 = (float)rx0 + 0.5f, Y0 = (float)ry0 + 0.5f;
         const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
+        SPLAT_DCHECK(start <= end);
 
         Blend<TRAIN> s;
         s.init();
@@ -459,6 +460,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                             ++at;
                         }
                     qt += __popc(v0) + 2u * __popc(v1) + 4u * __popc(v2);
+                    SPLAT_DCHECK(qt - qh <= (uint32_t)kQueue && at <= qt);
                     __syncwarp();   // the batch buffer is read: it may be refilled
                     bnext += kBatch;
                     if (lane == 0 && bnext + kBatch < end) issue_batch(bnext + kBatch, k);
@@ -471,6 +473,8 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                 if (lane < n) {
                     const uint32_t e = (qh + (uint32_t)lane) & (kQueue - 1);
                     const uint32_t r = s_qr[warp][e];
+                    SPLAT_DCHECK((int64_t)r < p.sc.n);
+                    SPLAT_DCHECK(!TRAIN || (s_qp[warp][TRAIN ? e : 0] >= start && s_qp[warp][TRAIN ? e : 0] < end));
                     const float4* src = reinterpret_cast<const float4*>(p.pack + r);
                     float4* dst = reinterpret_cast<float4*>(&S_PACK(warp, b, lane));
                     cp_async16(dst, src);
@@ -525,6 +529,7 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                         if (active && my_mask != 0u) {
                             const int idx = __ffs(my_mask) - 1;
                             my_mask &= my_mask - 1u;
+                            SPLAT_DCHECK(idx < ncur);
                             blend_candidate<TRAIN>(p, S_PACK(warp, b, idx), S_COL(warp, b, idx),
                                                    &s_rank[warp][b][idx], TRAIN ? s_pos[warp][TRAIN ? b : 0][idx] : 0u,
                                                    cx, cy, s, active, flagged);
@@ -617,6 +622,7 @@ __global__ void __launch_bounds__(FixShape<TRAIN>::kThreads, FixShape<TRAIN>::kM
     const uint32_t nfix = p.counters[2];
     for (uint32_t w = blockIdx.x; w < nfix; w += gridDim.x) {
         const uint32_t pix = p.fixup[w];
+        SPLAT_DCHECK(pix < (uint32_t)(p.width * p.height));
         const int px = (int)(pix % (uint32_t)p.width), py = (int)(pix / (uint32_t)p.width);
         const int tile = (py / kTile) * p.ntx + px / kTile;
         const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];

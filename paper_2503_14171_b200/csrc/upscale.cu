@@ -513,9 +513,11 @@ __global__ void __launch_bounds__(32 * UP_X4_WARPS, UP_X4_MINB) upscale_x4_kerne
 #pragma unroll
             for (int ry = 0; ry < 2; ++ry) {
                 const int row = clampi(n + ry, 0, in_h - 1) - y0;
+                SPLAT_DCHECK(row >= 0 && row < nrows && row < kX4SpanR);
 #pragma unroll
                 for (int cx = 0; cx < 3; ++cx) {
                     const int col = clampi(g - 1 + cx, 0, in_w - 1) - x0;
+                    SPLAT_DCHECK(col >= 0 && col < ncols && col < kX4SpanC);
                     const float4* p = reinterpret_cast<const float4*>(sb + ((size_t)row * kX4SpanC + col) * 12);
                     const float4 q0 = p[0], q1 = p[1], q2 = p[2];
                     float* r = rec[ry][cx];
@@ -681,6 +683,7 @@ __global__ void __launch_bounds__(32 * UP_X2_WARPS, UP_X2_MINB) upscale_x2_kerne
 #pragma unroll
             for (int cx = 0; cx < 4; ++cx) {
                 const int col = clampi(2 * g - 1 + cx, 0, in_w - 1) - x0;
+                SPLAT_DCHECK(col >= 0 && col < ncols && col < kX2SpanC && ra >= 0 && rb < nrows && rb < kX2SpanR);
                 const float4* pa = reinterpret_cast<const float4*>(sb + ((size_t)ra * kX2SpanC + col) * 12);
                 const float4* pb = reinterpret_cast<const float4*>(sb + ((size_t)rb * kX2SpanC + col) * 12);
                 const float4 a0 = pa[0], a1 = pa[1], a2 = pa[2];

@@ -138,15 +138,30 @@ def make_view(scene: DeviceScene, out_w: int, out_h: int, view=None) -> _lib.Vie
 class Frame:
     """Workspace of one render: pack, bboxes, pairs, sorted bins, tile ranges."""
 
-    def __init__(self, n: int, width: int, height: int, capacity: int, device):
+    GUARD_BYTE = 0xA5
+
+    def __init__(self, n: int, width: int, height: int, capacity: int, device, guard: int = 0):
         lib = _lib.load()
         self.n, self.width, self.height, self.capacity = n, width, height, int(capacity)
         self.nbytes = lib.splat_frame_workspace_bytes(n, width, height, self.capacity)
-        self.ws = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        self.guard = int(guard) // 256 * 256
+        if self.guard:   # test aid: canary bytes either side of the workspace (see guards_intact)
+            self._buf = torch.full((self.nbytes + 2 * self.guard,), self.GUARD_BYTE, dtype=torch.uint8,
+                                   device=device)
+            self.ws = self._buf[self.guard:self.guard + self.nbytes]
+        else:
+            self.ws = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
         self.ptrs = _lib.FramePtrsT()
         _lib.check(lib.splat_frame_pointers(_lib.ptr(self.ws), n, width, height, self.capacity,
                                             self.ptrs))
         self.counters().zero_()
+
+    def guards_intact(self) -> bool:
+        """True when no kernel wrote into the canary bytes around the workspace."""
+        if not self.guard:
+            return True
+        g = self.guard
+        return bool((self._buf[:g] == self.GUARD_BYTE).all()) and bool((self._buf[g + self.nbytes:] == self.GUARD_BYTE).all())
 
     def _view(self, ptr, count, dtype, shape):
         off = ptr - self.ws.data_ptr()
