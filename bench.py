@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--workload", default="render", choices=["render", "train"],
                     help="render: C3 frames/s (headline); train: C5 upscale-aware training step")
     ap.add_argument("--train-views", type=int, default=4, help="views per rank per training step (C5)")
+    ap.add_argument("--train-streams", type=int, default=4, help="C5 views in flight per rank (ViewTrainer streams)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
@@ -352,13 +353,14 @@ def train_workload(views_per_rank, world):
 TRAIN_METRIC = "upscale-aware training view-steps/s (C5: 1M splats, 480x270 render, x4 to 1920x1080, L1+SSIM)"
 
 
-def train_config(c, world, vpr):
+def train_config(c, world, vpr, streams=2):
     return {"workload": "c5: 1M-splat model (seed 5) fit to a 1M-splat target scene (seed 7); per view: "
                         "480x270 render with analytic gradients, x4 spline upscale to 1920x1080, "
                         "L1+SSIM (lambda 0.2) loss, backward through upscaler and rasterizer; "
                         "grads all-reduced over ranks, then Adam",
             "n_splats": c.n, "render": [c.width, c.height], "output": list(c.out_size),
-            "views_per_rank": vpr, "parallelism": f"view-DP x{world} + NCCL all_reduce(SUM) of the 9N fp32 rank-order gradient terms"}
+            "views_per_rank": vpr, "views_in_flight": streams,
+            "parallelism": f"view-DP x{world} + NCCL all_reduce(SUM) of the 9N fp32 rank-order gradient terms"}
 
 
 def cpu_reference_train_view(model, target_img, view, c):
@@ -388,7 +390,8 @@ def train_line(args, rank, world, local):
     mine = D.shard(views, rank, world)
     W, H = c.out_size
     targets = [render_forward(target_scene, W, H, view=v).color.clamp(0.0, 1.0).contiguous() for v in mine]
-    trainer = fit.ViewTrainer(model, (c.width, c.height), (W, H), mine, targets, ssim_weight=0.2)
+    trainer = fit.ViewTrainer(model, (c.width, c.height), (W, H), mine, targets, ssim_weight=0.2,
+                              streams=args.train_streams)
     for _ in range(args.warmup):
         trainer.step()
     torch.cuda.synchronize()
@@ -494,7 +497,7 @@ def train_line(args, rank, world, local):
         line = {"metric": TRAIN_METRIC, "value": value, "unit": "view-steps/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": train_config(c, world, vpr), "gpu_launches": int(launches),
+                "config": train_config(c, world, vpr, args.train_streams), "gpu_launches": int(launches),
                 "loss_last_step": [float(x) for x in losses[:, 0]],
                 "roofline": roof,
                 "cpu_baseline": cpu,

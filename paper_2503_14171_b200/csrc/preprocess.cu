@@ -805,6 +805,9 @@ int scene_refresh_impl(const splat_scene_t& s, void* const_buf, cudaStream_t str
 
 int launch_preprocess(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
                       cudaStream_t stream) {
+#ifdef TIMING_SKIP_PRE   // timing-only builds (tools/marginal.sh): measure a stage's marginal cost
+    if (L.n > 0) return SPLAT_OK;
+#endif
     uint32_t* counters = (uint32_t*)(ws + L.counters);
     SPLAT_CUDA_CHECK(cudaMemsetAsync(counters, 0, 4 * 4, stream));  // [4..] are sticky
     if (sc.n == 0) return SPLAT_OK;
@@ -817,6 +820,9 @@ int launch_preprocess(const SceneConst& sc, const ViewConst& vc, const FrameLayo
 }
 
 int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t stream) {
+#ifdef TIMING_SKIP_BIN
+    if (L.n > 0 && !(flags & (SPLAT_BIN_KEYS | SPLAT_BIN_OFFSETS))) return SPLAT_OK;
+#endif
     const bool with_offsets = flags & SPLAT_BIN_OFFSETS;
     uint32_t* counters = (uint32_t*)(ws + L.counters);
     uint32_t* ranges = (uint32_t*)(ws + L.ranges);

@@ -625,6 +625,7 @@ __global__ void __launch_bounds__(FixShape<TRAIN>::kThreads, FixShape<TRAIN>::kM
         SPLAT_DCHECK(pix < (uint32_t)(p.width * p.height));
         const int px = (int)(pix % (uint32_t)p.width), py = (int)(pix / (uint32_t)p.width);
         const int tile = (py / kTile) * p.ntx + px / kTile;
+        const int wrect = ((py % kTile) / 4) * 2 + (px % kTile) / 8;   // the pixel's 8x4 rectangle
         const uint32_t start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
         const float cx = (float)px + 0.5f, cy = (float)py + 0.5f;
         Blend<TRAIN> s;
@@ -635,17 +636,20 @@ __global__ void __launch_bounds__(FixShape<TRAIN>::kThreads, FixShape<TRAIN>::kM
         for (uint32_t seg = start; seg < end; seg += kFixSeg) {
             const int nseg = (int)min((uint32_t)kFixSeg, end - seg);
             // A: float32 screen; candidate i = tid * kFixPer + u keeps list order per thread
-            uint32_t rr[kFixPer];
+            // (candidates whose bbox misses the pixel's 8x4 rectangle -- binning's rect mask --
+            // cannot reach it: their pack is never loaded)
+            uint32_t rr[kFixPer], rm = 0;
 #pragma unroll
             for (int u = 0; u < kFixPer; ++u) {
                 const int i = tid * kFixPer + u;
                 rr[u] = i < nseg ? p.ranks[seg + i] : 0u;
+                if (i < nseg && ((p.rmask[seg + i] >> wrect) & 1u)) rm |= 1u << u;
             }
             uint32_t keepm = 0;
 #pragma unroll
             for (int u = 0; u < kFixPer; ++u) {
                 const int i = tid * kFixPer + u;
-                if (i < nseg) {
+                if ((rm >> u) & 1u) {
                     const PackF g = p.pack[rr[u]];
                     float al, gax, gay, gaxy, rel;
                     if (eval_fast(g, cx, cy, al, gax, gay, gaxy, rel) != kCulled) keepm |= 1u << u;
@@ -770,7 +774,9 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
         fixup_kernel<true><<<FIX_GRID, FixShape<true>::kThreads, sizeof(FixShared<true>), stream>>>(a); note_launch();
     } else {
         raster_fwd_kernel<false><<<grid_inf, kRasterThreads, 0, stream>>>(a); note_launch();
+#ifndef TIMING_SKIP_FIX
         fixup_kernel<false><<<FIX_GRID, FixShape<false>::kThreads, sizeof(FixShared<false>), stream>>>(a); note_launch();
+#endif
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
