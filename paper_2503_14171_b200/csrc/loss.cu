@@ -60,8 +60,10 @@ __global__ void __launch_bounds__(256, 3) ssim_stats_kernel(const float* __restr
     double* s_h = reinterpret_cast<double*>(sm + 2 * (size_t)kHalo * (kHalo + 1) * 4);   // [5][kHalo][kS]
     __shared__ double s_red[8];
     const int tid = threadIdx.x;
-    const int X0 = blockIdx.x * kS, Y0 = blockIdx.y * kS;
-    const int ch = blockIdx.z;
+    // the three channel CTAs of a tile are adjacent in launch order, so the interleaved
+    // (H, W, 3) pred / target sectors one of them fetches are L2 hits for the other two
+    const int ch = blockIdx.x % 3, bx = blockIdx.x / 3, gx = gridDim.x / 3;
+    const int X0 = bx * kS, Y0 = blockIdx.y * kS;
     double local = 0.0;
     // load the channel tile with a zero halo (zero padding: correlate1d mode="constant")
     for (int e = tid; e < kHalo * kHalo; e += 256) {
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(256, 3) ssim_stats_kernel(const float* __restr
     if (tid == 0) {
         double t = 0.0;
         for (int i = 0; i < 8; ++i) t += s_red[i];
-        part_ssim[((size_t)ch * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+        part_ssim[((size_t)ch * gridDim.y + blockIdx.y) * gx + bx] = t;
     }
 }
 
@@ -176,8 +178,10 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
     __shared__ float s_h[3][kHalo][kS + 1];
     __shared__ float s_red[8];
     const int tid = threadIdx.x;
-    const int X0 = blockIdx.x * kS, Y0 = blockIdx.y * kS;
-    const int ch = blockIdx.z;
+    // the three channel CTAs of a tile are adjacent in launch order, so the interleaved
+    // (H, W, 3) pred / target sectors one of them fetches are L2 hits for the other two
+    const int ch = blockIdx.x % 3, bx = blockIdx.x / 3, gx = gridDim.x / 3;
+    const int X0 = bx * kS, Y0 = blockIdx.y * kS;
     float local = 0.f;
     for (int e = tid; e < kHalo * kHalo; e += 256) {
         const int r = e / kHalo, c = e - r * kHalo;
@@ -264,7 +268,7 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
     if (tid == 0) {
         float t = 0.f;
         for (int i = 0; i < 8; ++i) t += s_red[i];
-        part_l1[((size_t)ch * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+        part_l1[((size_t)ch * gridDim.y + blockIdx.y) * gx + bx] = t;
     }
 }
 
@@ -385,7 +389,7 @@ int loss_impl(const float* pred, const float* target, int w, int h, double lam, 
     const double inner = (double)(h - 2 * kR) * (double)(w - 2 * kR);
     const double size = (double)w * h * 3;
     const double gscale = 1.0 / (inner * 3.0);
-    dim3 grid(gx, gy, 3);
+    dim3 grid(3 * gx, gy);   // channel fastest (see ssim_stats_kernel)
     if (lam > 0.0) {
         ssim_stats_kernel<<<grid, 256, kStatsSmem, stream>>>(pred, target, w, h, gscale, coef, part_ssim); note_launch();
     } else {
