@@ -7,7 +7,8 @@
 * ViewTrainer.step inside a real process group: the all-reduced step equals the
   single-process step over all views (float32 summation order only) and the
   oracle's sum of per-view gradients (1e-3 relative, SURVEY 8(e);
-  reference: raster_backward.py:116-124, fit.py:188-223).
+  reference: raster_backward.py:116-124, fit.py:188-223);
+* three ranks' view shards render bitwise what one process renders for the batch.
 """
 
 import json
@@ -122,3 +123,53 @@ def test_view_trainer_step_in_a_real_process_group(oracle):
     for f in FIELDS:
         assert rel_err(g0[f], ref[f]) < 1e-3, (f, rel_err(g0[f], ref[f]))
     torch.cuda.synchronize()
+
+
+def _render_rank(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_14171_b200 import distributed as D
+        from paper_2503_14171_b200.pipeline import render_upscale_views
+        from paper_2503_14171_b200.scenes import random_views, synthetic_scene
+        sc = synthetic_scene(30000, 320, 180, (0.5, 2.5), seed=5)
+        views = random_views(9, 320, 180, seed=4)
+        lo, hi = D.shard_bounds(len(views), rank, world)
+        out = render_upscale_views(sc, 320, 180, views[lo:hi], factor=4.0, slots=3)
+        q.put((rank, lo, out.cpu().numpy()))
+    except Exception as e:
+        q.put((rank, -1, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_view_sharded_render_is_invariant_to_world_size():
+    """The reference's output never depends on its worker count (raster_forward.py:181-186,
+    pkg/tests/test_raster_forward.py:200-207); here: the frames three ranks render for their
+    shards of a 9-view batch are bitwise the single-process batch."""
+    import torch
+    import torch.multiprocessing as mp
+    from paper_2503_14171_b200.distributed import free_port
+    from paper_2503_14171_b200.pipeline import render_upscale_views
+    from paper_2503_14171_b200.scenes import random_views, synthetic_scene
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_render_rank, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in procs), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+    for r in res:
+        assert r[1] >= 0, r[2]
+    sharded = np.concatenate([r[2] for r in res])
+    sc = synthetic_scene(30000, 320, 180, (0.5, 2.5), seed=5)
+    whole = render_upscale_views(sc, 320, 180, random_views(9, 320, 180, seed=4), factor=4.0, slots=3)
+    torch.cuda.synchronize()
+    assert sharded.shape == tuple(whole.shape)
+    assert np.array_equal(sharded, whole.cpu().numpy())
