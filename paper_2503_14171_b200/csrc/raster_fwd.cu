@@ -512,12 +512,25 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                 }
                 int cnt_max = 0;
                 uint32_t my_mask = 0;   // this lane's group: candidates of the chunk, walked low to high
+#if RASTER_STATS
+                int cnt_sum = 0;
+#endif
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
                     const uint32_t mq = __ballot_sync(0xffffffffu, (gmask >> qq) & 1u);
                     cnt_max = max(cnt_max, __popc(mq));
                     if (qq == q) my_mask = mq;
+#if RASTER_STATS
+                    cnt_sum += __popc(mq);
+#endif
                 }
+#if RASTER_STATS   // tools/raster_stats.py: chunks, steps, group entries (counters[8..13] as u64)
+                if (lane == 0) {
+                    atomicAdd((unsigned long long*)&p.counters[8], 1ull);
+                    atomicAdd((unsigned long long*)&p.counters[10], (unsigned long long)cnt_max);
+                    atomicAdd((unsigned long long*)&p.counters[12], (unsigned long long)cnt_sum);
+                }
+#endif
                 __syncwarp();
                 // RASTER_UNROLL steps per iteration in inference (a step with an empty list is a
                 // no-op, so the tail needs no guard): less loop-back and termination-vote
@@ -526,6 +539,12 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                 for (int k = 0; k < cnt_max; k += kU) {
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
+#if RASTER_STATS
+                        {
+                            const uint32_t ev = __ballot_sync(0xffffffffu, active && my_mask != 0u);
+                            if (lane == 0) atomicAdd((unsigned long long*)&p.counters[14], (unsigned long long)__popc(ev));
+                        }
+#endif
                         if (active && my_mask != 0u) {
                             const int idx = __ffs(my_mask) - 1;
                             my_mask &= my_mask - 1u;
