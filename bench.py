@@ -659,8 +659,9 @@ def render_line(args, rank, world, local):
     roof_up = None
     if stage:
         r_ms = stage["raster"]
-        roof = {"kernel": "raster_fwd_kernel + fixup_kernel (per view)", "bound": "fp32",
-                "measured": f"CUDA events per stage, single-stream pass over {len(kviews)} views",
+        roof = {"kernel": "raster_fwd_kernel (splat_rasterize with the fix-up deferred; per view)", "bound": "fp32",
+                "measured": f"CUDA events around the raster kernel on its stream, single-stream pass over "
+                            f"{len(kviews)} views (the exact fix-up is timed as its own stage)",
                 "achieved": raster_flops / (r_ms * 1e-3) / 1e12,
                 "peak": fp32_peak, "unit": "TFLOP/s", "frac": raster_flops / (r_ms * 1e-3) / 1e12 / fp32_peak,
                 "traffic": traffic.get("raster_fwd_kernel"),

@@ -144,10 +144,19 @@ int splat_prepare_view(const void *scene_const, int64_t n, const splat_view_t *v
 int splat_bin_tiles(int64_t n, int width, int height, void *workspace, size_t ws_bytes,
                     int64_t pair_capacity, int flags, void *stream);
 /* Rasterizer + exact fix-up pass alone, on a frame already prepared and binned
- * by the two calls above (render_forward = prepare_view + bin_tiles + rasterize). */
+ * by the two calls above (render_forward = prepare_view + bin_tiles + rasterize).
+ * `train`: bit 0 = training mode (float64 state); bit 1 (SPLAT_RASTER_DEFER_FIXUP) =
+ * launch the raster kernel only, the caller then runs splat_fixup on the same stream
+ * (stage timing: the two kernels have different rooflines). */
+#define SPLAT_RASTER_DEFER_FIXUP 2
 int splat_rasterize(const void *scene_const, int64_t n, const splat_view_t *view, int width,
                     int height, int train, const splat_gimg_t *out, void *workspace, size_t ws_bytes,
                     int64_t pair_capacity, void *stream);
+/* The exact float64 re-render of the pixels splat_rasterize(..., train | SPLAT_RASTER_DEFER_FIXUP)
+ * flagged (the reference's acc = acc + alpha (1 - acc) chain, _kernels.py:88-111). */
+int splat_fixup(const void *scene_const, int64_t n, const splat_view_t *view, int width, int height,
+                int train, const splat_gimg_t *out, void *workspace, size_t ws_bytes, int64_t pair_capacity,
+                void *stream);
 /* Exact float64 RenderPack of a view (prepare_scene means/conics/sigmas,
  * raster_forward.py:86-102), rank order: pack64 (n,6) = mx,my,a,b,c,sigma;
  * colors64 (n,3) may be NULL.  Inspection only (the rasterizer uses float32). */

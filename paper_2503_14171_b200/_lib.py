@@ -74,6 +74,7 @@ SIGNATURES = {
     "splat_grad_accumulate": (I32, [P, P, I64, P]),
     "splat_render_points": (I32, [P, P, P, I64, P, P, I64, ctypes.POINTER(D), P, P, P]),
     "splat_project_3d": (I32, [I64, P, P, P, P, ctypes.POINTER(CameraT), P, P, P, P, P, P]),
+    "splat_fixup": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32, ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_rasterize": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
                               ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_view_pack64": (I32, [P, I64, ctypes.POINTER(ViewT), P, P]),

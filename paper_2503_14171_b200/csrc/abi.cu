@@ -176,11 +176,22 @@ int splat_rasterize(const void* scene_const, int64_t n, const splat_view_t* view
                     int64_t pair_capacity, void* stream) {
     int rc = check_dims(width, height);
     if (rc) return rc;
-    if (train && !out->state) return set_error(SPLAT_ERR_PARAMETER, "train mode needs the state buffer");
+    const bool tr = train & 1, defer = train & SPLAT_RASTER_DEFER_FIXUP;
+    if (tr && !out->state) return set_error(SPLAT_ERR_PARAMETER, "train mode needs the state buffer");
     FrameLayout L = frame_layout(n, width, height, pair_capacity);
     if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
     return launch_raster_forward(scene_const_view(scene_const, n), make_view_const(*view), L,
-                                 (char*)workspace, *out, train != 0, (cudaStream_t)stream);
+                                 (char*)workspace, *out, tr, (cudaStream_t)stream, !defer);
+}
+int splat_fixup(const void* scene_const, int64_t n, const splat_view_t* view, int width, int height, int train,
+                const splat_gimg_t* out, void* workspace, size_t ws_bytes, int64_t pair_capacity, void* stream) {
+    int rc = check_dims(width, height);
+    if (rc) return rc;
+    if ((train & 1) && !out->state) return set_error(SPLAT_ERR_PARAMETER, "train mode needs the state buffer");
+    FrameLayout L = frame_layout(n, width, height, pair_capacity);
+    if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    return launch_fixup(scene_const_view(scene_const, n), make_view_const(*view), L, (char*)workspace, *out,
+                        (train & 1) != 0, (cudaStream_t)stream);
 }
 
 size_t splat_upscale_plan_bytes(int in_w, int in_h, int out_w, int out_h) {

@@ -66,6 +66,8 @@ int launch_preprocess(const SceneConst& sc, const ViewConst& vc, const FrameLayo
                       cudaStream_t stream);
 int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t stream);
 int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
-                          const splat_gimg_t& out, bool train, cudaStream_t stream);
+                          const splat_gimg_t& out, bool train, cudaStream_t stream, bool with_fixup = true);
+int launch_fixup(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
+                 const splat_gimg_t& out, bool train, cudaStream_t stream);
 
 }  // namespace splat

@@ -742,10 +742,9 @@ __global__ void __launch_bounds__(FixShape<TRAIN>::kThreads, FixShape<TRAIN>::kM
     }
 }
 
-}  // namespace
 
-int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
-                          const splat_gimg_t& out, bool train, cudaStream_t stream) {
+static RasterArgs raster_args(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
+                              const splat_gimg_t& out) {
     RasterArgs a;
     a.sc = sc;
     a.vc = vc;
@@ -764,12 +763,16 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
     a.state = out.state;
     a.fixup = (uint32_t*)(ws + L.fixup);
     a.counters = (uint32_t*)(ws + L.counters);
-    struct Grids {
-        int inf, train;
-    };
-    static PerDevice<Grids> grids;
-    Grids gr{};
-    const int rc = grids.get(gr, [](Grids& g) {
+    return a;
+}
+
+struct RasterGrids {
+    int inf, train;
+};
+
+static int raster_grids(RasterGrids& gr) {
+    static PerDevice<RasterGrids> grids;
+    return grids.get(gr, [](RasterGrids& g) {
         int per_sm = 0, sms = 148;
         const int e = device_sms(sms);
         if (e != SPLAT_OK) return e;
@@ -783,22 +786,43 @@ int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const Frame
                                               (int)sizeof(FixShared<true>)));
         return SPLAT_OK;
     });
+}
+
+}  // namespace
+
+// The exact re-render of the pixels the raster kernel flagged (counters[2] of the frame).
+int launch_fixup(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws, const splat_gimg_t& out,
+                 bool train, cudaStream_t stream) {
+    RasterGrids gr{};
+    const int rc = raster_grids(gr);
     if (rc != SPLAT_OK) return rc;
-    const int grid_inf = gr.inf, grid_train = gr.train;
-    const int ntiles = L.ntx * L.nty;
-    // counters[2] = fix-up pixels, counters[3] = work-unit cursor of the persistent raster
-    SPLAT_CUDA_CHECK(cudaMemsetAsync(a.counters + 2, 0, 8, stream));
+    RasterArgs a = raster_args(sc, vc, L, ws, out);
     if (train) {
-        raster_fwd_kernel<true><<<grid_train, kRasterThreads, 0, stream>>>(a); note_launch();
         fixup_kernel<true><<<FIX_GRID, FixShape<true>::kThreads, sizeof(FixShared<true>), stream>>>(a); note_launch();
     } else {
-        raster_fwd_kernel<false><<<grid_inf, kRasterThreads, 0, stream>>>(a); note_launch();
 #ifndef TIMING_SKIP_FIX
         fixup_kernel<false><<<FIX_GRID, FixShape<false>::kThreads, sizeof(FixShared<false>), stream>>>(a); note_launch();
 #endif
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
+}
+
+int launch_raster_forward(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L, char* ws,
+                          const splat_gimg_t& out, bool train, cudaStream_t stream, bool with_fixup) {
+    RasterGrids gr{};
+    const int rc = raster_grids(gr);
+    if (rc != SPLAT_OK) return rc;
+    RasterArgs a = raster_args(sc, vc, L, ws, out);
+    // counters[2] = fix-up pixels, counters[3] = work-unit cursor of the persistent raster
+    SPLAT_CUDA_CHECK(cudaMemsetAsync(a.counters + 2, 0, 8, stream));
+    if (train) {
+        raster_fwd_kernel<true><<<gr.train, kRasterThreads, 0, stream>>>(a); note_launch();
+    } else {
+        raster_fwd_kernel<false><<<gr.inf, kRasterThreads, 0, stream>>>(a); note_launch();
+    }
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return with_fixup ? launch_fixup(sc, vc, L, ws, out, train, stream) : SPLAT_OK;
 }
 
 }  // namespace splat

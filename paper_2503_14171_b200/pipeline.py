@@ -23,7 +23,8 @@ from .device import to_device
 from .raster_forward import Frame, GradientImage, make_view
 from .spline import check_output, output_size, upscale_plan
 
-STAGES = ("prepare", "bin", "raster", "upscale")
+STAGES = ("prepare", "bin", "raster", "fixup", "upscale")
+DEFER_FIXUP = 2   # splat_rasterize flag (SPLAT_RASTER_DEFER_FIXUP): the fix-up runs as its own call
 
 
 class _Slot:
@@ -126,15 +127,22 @@ class ViewPipeline:
                                            fw.capacity, 0, st))
             if ev is not None:
                 marks[2].record(slot.stream)
-            _lib.check(lib.splat_rasterize(_lib.ptr(ds.const), ds.n, cv, self.width, self.height, 0,
-                                           slot.gimg, _lib.ptr(fw.ws), fw.nbytes, fw.capacity, st))
-            if ev is not None:
+            if ev is None:   # raster kernel + exact fix-up in one call
+                _lib.check(lib.splat_rasterize(_lib.ptr(ds.const), ds.n, cv, self.width, self.height, 0,
+                                               slot.gimg, _lib.ptr(fw.ws), fw.nbytes, fw.capacity, st))
+            else:            # stage timing: the two kernels separately (different rooflines)
+                _lib.check(lib.splat_rasterize(_lib.ptr(ds.const), ds.n, cv, self.width, self.height,
+                                               DEFER_FIXUP, slot.gimg, _lib.ptr(fw.ws), fw.nbytes, fw.capacity,
+                                               st))
                 marks[3].record(slot.stream)
+                _lib.check(lib.splat_fixup(_lib.ptr(ds.const), ds.n, cv, self.width, self.height, 0, slot.gimg,
+                                           _lib.ptr(fw.ws), fw.nbytes, fw.capacity, st))
+                marks[4].record(slot.stream)
             _lib.check(lib.splat_upscale_forward(_lib.ptr(slot.img.planes), self.width, self.height,
                                                  _lib.ptr(dst), self.out_w, self.out_h, 1,
                                                  _lib.ptr(self.plan), st))
             if ev is not None:
-                marks[4].record(slot.stream)
+                marks[5].record(slot.stream)
                 ev.append(marks)
             if host_out is not None:
                 done = torch.cuda.Event()

@@ -62,3 +62,23 @@ def test_batched_views_api():
     assert tuple(out.shape) == (6, 144, 256, 3)
     for i, v in enumerate(views):
         assert torch.equal(out[i], P.upscale_spline(P.render_forward(sc, 128, 72, view=v), 2.0))
+
+
+def test_stage_timed_pipeline_is_bitwise_the_fused_one():
+    """Stage timing runs the raster kernel and the exact fix-up as separate calls
+    (splat_rasterize(..., SPLAT_RASTER_DEFER_FIXUP) + splat_fixup): same frames, bit for bit,
+    on a scene whose termination boundary exercises the fix-up."""
+    import torch
+    import paper_2503_14171_b200 as P
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    sc = P.synthetic_scene(60000, 320, 180, (0.5, 2.5), seed=9)
+    views = P.random_views(4, 320, 180, seed=6)
+    a = ViewPipeline(sc, 320, 180, factor=4.0, slots=1, views_for_capacity=views)
+    b = ViewPipeline(sc, 320, 180, factor=4.0, slots=1, capacity=a.capacity)
+    b.enable_stage_timing(True)
+    fa, fb = a.render(views, keep=True), b.render(views, keep=True)
+    torch.cuda.synchronize()
+    assert set(b.stage_times_ms()) == {"prepare", "bin", "raster", "fixup", "upscale"}
+    for x, y in zip(fa, fb):
+        assert torch.equal(x, y)
+    assert int(a.slots[0].frame.counters()[2]) > 0   # the last view did flag pixels for the fix-up
