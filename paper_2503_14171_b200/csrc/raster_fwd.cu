@@ -777,6 +777,9 @@ static int raster_grids(RasterGrids& gr) {
         const int e = device_sms(sms);
         if (e != SPLAT_OK) return e;
         SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<false>, kRasterThreads, 0));
+#ifdef RASTER_GRID_PER_SM   // fewer persistent CTAs than fit: room for other streams' kernels beside them
+        per_sm = min(per_sm, RASTER_GRID_PER_SM);
+#endif
         g.inf = max(per_sm, 1) * sms;
         SPLAT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_fwd_kernel<true>, kRasterThreads, 0));
         g.train = max(per_sm, 1) * sms;
