@@ -13,6 +13,9 @@
 //                    append order and [start, end) ranges (bin_tiles,
 //                    raster_forward.py:136-149); see "tile binning" below.
 #include <cmath>
+#ifdef TIMING_SKIP_BIN
+#include <set>
+#endif
 
 #include "kernels.cuh"
 
@@ -820,8 +823,11 @@ int launch_preprocess(const SceneConst& sc, const ViewConst& vc, const FrameLayo
 }
 
 int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t stream) {
-#ifdef TIMING_SKIP_BIN
-    if (L.n > 0 && !(flags & (SPLAT_BIN_KEYS | SPLAT_BIN_OFFSETS))) return SPLAT_OK;
+#ifdef TIMING_SKIP_BIN   // bin each workspace once, then reuse its lists (tools/same_view_probe.py)
+    {
+        static std::set<const char*> binned;
+        if (L.n > 0 && !(flags & (SPLAT_BIN_KEYS | SPLAT_BIN_OFFSETS)) && !binned.insert(ws).second) return SPLAT_OK;
+    }
 #endif
     const bool with_offsets = flags & SPLAT_BIN_OFFSETS;
     uint32_t* counters = (uint32_t*)(ws + L.counters);
