@@ -141,6 +141,9 @@ int splat_prepare_view(const void *scene_const, int64_t n, const splat_view_t *v
 /* SPLAT_BIN_ATOMIC forces the binning path used for very large tile grids
  * (per-pair global atomics + per-tile sort); same output, for testing. */
 #define SPLAT_BIN_ATOMIC 4
+/* SPLAT_BIN_COUNT_ONLY stops after the per-tile counts: counters[0] = the pair count
+ * (capacity calibration; no pairs are written, so any pair_capacity is accepted). */
+#define SPLAT_BIN_COUNT_ONLY 8
 int splat_bin_tiles(int64_t n, int width, int height, void *workspace, size_t ws_bytes,
                     int64_t pair_capacity, int flags, void *stream);
 /* Rasterizer + exact fix-up pass alone, on a frame already prepared and binned

@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
         write_range(t, tile_start, tile_count, ranges, cap);
     const int64_t nblk = (n + kBinBlock - 1) / kBinBlock;
+    const float inv_ntx = 1.0f / (float)ntx;
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         short4 bb[kBinRPT];
 #pragma unroll
@@ -473,10 +474,13 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
                 if ((int64_t)pos < cap) {
                     if (keys) keys[pos] = (uint32_t)t;
                     const short4 b = bboxes[v];   // the block's boxes: L1 / L2 hits
-                    rmask[pos] = (uint8_t)rect_mask(b, t % ntx, t / ntx);
+                    // t / ntx without an integer division: (t + 0.5) / ntx is >= 0.5 / ntx away
+                    // from an integer, far beyond the float32 error for t < 2^16
+                    const int ty = __float2int_rd(((float)t + 0.5f) * inv_ntx), tx = t - ty * ntx;
+                    rmask[pos] = (uint8_t)rect_mask(b, tx, ty);
                     if (slot_pos) {   // training: emission slot -> list position (see slot_map_kernel)
                         const int tx0 = b.x >> 4, ty0 = b.z >> 4, nx = ((b.y - 1) >> 4) - tx0 + 1;
-                        const int64_t e = (int64_t)offsets[v] + (t / ntx - ty0) * nx + (t % ntx - tx0);
+                        const int64_t e = (int64_t)offsets[v] + (ty - ty0) * nx + (tx - tx0);
                         if (e < cap) slot_pos[e] = pos;
                     }
                 }
@@ -885,6 +889,10 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
             note_launch();
             exclusive_scan_u32(tile_count, tile_start, ntiles, scan_tmp, &counters[0], stream);
         }
+        if (flags & SPLAT_BIN_COUNT_ONLY) {   // counters[0] holds the pair count
+            SPLAT_CUDA_CHECK(cudaGetLastError());
+            return SPLAT_OK;
+        }
         fill_rows_kernel<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, pre, part,
                                                                   tile_start, tile_count, ranges, L.cap, ranks,
                                                                   keys, counters, (const uint32_t*)(ws + L.offsets),
@@ -898,6 +906,10 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         SPLAT_CUDA_CHECK(cudaMemsetAsync(tile_count, 0, (size_t)ntiles * 4, stream));
         count_tiles_kernel<<<blocks, 256, 0, stream>>>(L.n, bboxes, touched, L.ntx, tile_count); note_launch();
         exclusive_scan_u32(tile_count, tile_start, ntiles, scan_tmp, &counters[0], stream);
+        if (flags & SPLAT_BIN_COUNT_ONLY) {
+            SPLAT_CUDA_CHECK(cudaGetLastError());
+            return SPLAT_OK;
+        }
         uint32_t* cursor = (uint32_t*)(ws + L.cursor);
         init_ranges_kernel<<<ceil_div(ntiles, 256), 256, 0, stream>>>(ntiles, tile_start, tile_count, ranges,
                                                                       cursor, L.cap, counters); note_launch();

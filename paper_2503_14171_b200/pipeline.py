@@ -20,7 +20,7 @@ import torch
 from . import _lib
 from .core import DimensionError
 from .device import to_device
-from .raster_forward import Frame, GradientImage, make_view
+from .raster_forward import BIN_COUNT_ONLY, Frame, GradientImage, make_view
 from .spline import check_output, output_size, upscale_plan
 
 STAGES = ("prepare", "bin", "raster", "fixup", "upscale")
@@ -71,7 +71,7 @@ class ViewPipeline:
             _lib.check(lib.splat_prepare_view(_lib.ptr(ds.const), ds.n, cv, self.width, self.height,
                                               _lib.ptr(frame.ws), frame.nbytes, frame.capacity, st))
             _lib.check(lib.splat_bin_tiles(ds.n, self.width, self.height, _lib.ptr(frame.ws), frame.nbytes,
-                                           frame.capacity, 0, st))
+                                           frame.capacity, BIN_COUNT_ONLY, st))
             totals[i] = frame.counters()[0].to(torch.int64)
         return int(int(totals.max()) * margin) + 4096
 

@@ -31,7 +31,7 @@ __all__ = ["GradientImage", "RenderPack", "TileBins", "Frame", "sort_by_depth", 
            "tile_grid", "bin_tiles", "render_forward", "render_at_points", "make_view"]
 
 PLANES = ("color", "d_dx", "d_dy", "d_dxdy")
-BIN_OFFSETS, BIN_KEYS, BIN_ATOMIC = 1, 2, 4   # splat_bin_tiles flags (include/splat_b200.h)
+BIN_OFFSETS, BIN_KEYS, BIN_ATOMIC, BIN_COUNT_ONLY = 1, 2, 4, 8   # splat_bin_tiles flags (include/splat_b200.h)
 ALPHAS = ("alpha", "alpha_dx", "alpha_dy", "alpha_dxdy")
 
 
