@@ -657,6 +657,7 @@ def render_line(args, rank, world, local):
         pass
     roof = None
     roof_up = None
+    roof_issue = None
     if stage:
         r_ms = stage["raster"]
         roof = {"kernel": "raster_fwd_kernel (splat_rasterize with the fix-up deferred; per view)", "bound": "fp32",
@@ -670,7 +671,15 @@ def render_line(args, rank, world, local):
                 "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (median SM clock in run)",
                 "ncu_utilisation": util.get("raster_fwd_kernel"),
                 "note": "the SURVEY 8(d) FLOP count omits the certified-decision arithmetic, culling and "
-                        "blend bookkeeping; the kernel is issue-bound (see ncu_utilisation)"}
+                        "blend bookkeeping; the kernel is issue-bound (see ncu_utilisation, roofline_issue)"}
+        inst = (util.get("raster_fwd_kernel") or {}).get("inst_executed")
+        if inst:   # the bound the kernel actually meets: warp-instruction issue (4 schedulers per SM)
+            issue_peak = NUM_SMS * 4 * sm_mhz * 1e6
+            roof_issue = {"kernel": "raster_fwd_kernel", "bound": "issue", "unit": "G warp-instructions/s",
+                          "achieved": inst / (r_ms * 1e-3) / 1e9, "peak": issue_peak / 1e9,
+                          "frac": inst / (r_ms * 1e-3) / issue_peak, "instructions_per_launch": inst,
+                          "source": "smsp__inst_executed.sum of one C3 launch (profiles/r02/ncu_summary.txt) over "
+                                    "the stage time measured here; peak = 148 SM x 4 schedulers x 1 issue/clock"}
     if rank == 0:
         # steady state: back-to-back launches over 4 distinct sources and frames (working set
         # 4 x 124 MB at C3/C4 >> the 126 MB L2), so each frame's write-back is paid in the window
@@ -705,7 +714,8 @@ def render_line(args, rank, world, local):
                 "data": "synthetic", "config": cfg,
                 "mpix_per_s": value * vpf * OW * OH / 1e6,
                 "stage_ms_per_view": stage, "gpu_launches": int(launches),
-                "roofline": roof, "roofline_upscale": roof_up, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "roofline_upscale": roof_up, "roofline_issue": roof_issue,
+                "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clk}
         return line
     return None

@@ -78,7 +78,7 @@ def main():
             traffic[tag] = int(by)
             util[tag] = {k: v[k] for k in ("issue_slots_busy_pct", "fma_pipe_pct", "alu_pipe_pct", "xu_pipe_pct",
                                           "lsu_pipe_pct", "shared_wavefronts_pct", "warps_active_pct", "dram_pct",
-                                          "duration_us") if k in v}
+                                          "duration_us", "inst_executed") if k in v}
     traffic["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full capture per "
                         "kernel (profiles/r02/ncu_summary.txt); the upscalers are captured in steady state with "
                         "--cache-control none (20th launch of a 4-buffer rotation), the others with ncu's default "
