@@ -672,7 +672,7 @@ def render_line(args, rank, world, local):
                 "ncu_utilisation": util.get("raster_fwd_kernel"),
                 "note": "the SURVEY 8(d) FLOP count omits the certified-decision arithmetic, culling and "
                         "blend bookkeeping; the kernel is issue-bound (see ncu_utilisation, roofline_issue)"}
-        inst = (util.get("raster_fwd_kernel") or {}).get("inst_executed")
+        inst = (util.get("raster_fwd_kernel") or {}).get("inst_executed") if args.config == "c3" else None
         if inst:   # the bound the kernel actually meets: warp-instruction issue (4 schedulers per SM)
             issue_peak = NUM_SMS * 4 * sm_mhz * 1e6
             roof_issue = {"kernel": "raster_fwd_kernel", "bound": "issue", "unit": "G warp-instructions/s",
