@@ -135,6 +135,7 @@ int splat_prepare_view(const void* scene_const, int64_t n, const splat_view_t* v
     if (rc) return rc;
     FrameLayout L = frame_layout(n, width, height, pair_capacity);
     if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    if ((uintptr_t)workspace & 255) return set_error(SPLAT_ERR_PARAMETER, "frame workspace must be 256-byte aligned");
     return launch_preprocess(scene_const_view(scene_const, n), make_view_const(*view), L, (char*)workspace,
                              (cudaStream_t)stream);
 }
@@ -145,6 +146,7 @@ int splat_bin_tiles(int64_t n, int width, int height, void* workspace, size_t ws
     if (rc) return rc;
     FrameLayout L = frame_layout(n, width, height, pair_capacity);
     if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    if ((uintptr_t)workspace & 255) return set_error(SPLAT_ERR_PARAMETER, "frame workspace must be 256-byte aligned");
     return launch_binning(L, (char*)workspace, flags, (cudaStream_t)stream);
 }
 
@@ -162,6 +164,7 @@ int splat_render_forward(const void* scene_const, int64_t n, const splat_view_t*
     if (train && !out->state) return set_error(SPLAT_ERR_PARAMETER, "train mode needs the state buffer");
     FrameLayout L = frame_layout(n, width, height, pair_capacity);
     if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    if ((uintptr_t)workspace & 255) return set_error(SPLAT_ERR_PARAMETER, "frame workspace must be 256-byte aligned");
     cudaStream_t s = (cudaStream_t)stream;
     SceneConst sc = scene_const_view(scene_const, n);
     ViewConst vc = make_view_const(*view);
@@ -180,6 +183,7 @@ int splat_rasterize(const void* scene_const, int64_t n, const splat_view_t* view
     if (tr && !out->state) return set_error(SPLAT_ERR_PARAMETER, "train mode needs the state buffer");
     FrameLayout L = frame_layout(n, width, height, pair_capacity);
     if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    if ((uintptr_t)workspace & 255) return set_error(SPLAT_ERR_PARAMETER, "frame workspace must be 256-byte aligned");
     return launch_raster_forward(scene_const_view(scene_const, n), make_view_const(*view), L,
                                  (char*)workspace, *out, tr, (cudaStream_t)stream, !defer);
 }
@@ -190,6 +194,7 @@ int splat_fixup(const void* scene_const, int64_t n, const splat_view_t* view, in
     if ((train & 1) && !out->state) return set_error(SPLAT_ERR_PARAMETER, "train mode needs the state buffer");
     FrameLayout L = frame_layout(n, width, height, pair_capacity);
     if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    if ((uintptr_t)workspace & 255) return set_error(SPLAT_ERR_PARAMETER, "frame workspace must be 256-byte aligned");
     return launch_fixup(scene_const_view(scene_const, n), make_view_const(*view), L, (char*)workspace, *out,
                         (train & 1) != 0, (cudaStream_t)stream);
 }
@@ -221,6 +226,7 @@ int splat_render_backward(const void* scene_const, const splat_scene_t* scene, c
         return set_error(SPLAT_ERR_PARAMETER, "backward needs a training-mode forward (state + last)");
     FrameLayout L = frame_layout(scene->n, width, height, pair_capacity);
     if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    if ((uintptr_t)workspace & 255) return set_error(SPLAT_ERR_PARAMETER, "frame workspace must be 256-byte aligned");
     if (bwd_bytes < backward_workspace_bytes_impl(scene->n, pair_capacity))
         return set_error(SPLAT_ERR_PARAMETER, "backward workspace too small");
     return launch_raster_backward(scene_const_view(scene_const, scene->n), *scene, make_view_const(*view), L,
@@ -238,6 +244,7 @@ int splat_render_backward_rank(const void* scene_const, const splat_scene_t* sce
         return set_error(SPLAT_ERR_PARAMETER, "backward needs a training-mode forward (state + last)");
     FrameLayout L = frame_layout(scene->n, width, height, pair_capacity);
     if (ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+    if ((uintptr_t)workspace & 255) return set_error(SPLAT_ERR_PARAMETER, "frame workspace must be 256-byte aligned");
     if (bwd_bytes < backward_workspace_bytes_impl(scene->n, pair_capacity))
         return set_error(SPLAT_ERR_PARAMETER, "backward workspace too small");
     return launch_raster_backward(scene_const_view(scene_const, scene->n), *scene, make_view_const(*view), L,
@@ -275,6 +282,11 @@ int splat_upscale_forward(const float* src, int in_w, int in_h, float* out, int 
     if (out_w < in_w || out_h < in_h)
         return set_error(SPLAT_ERR_SCALE, "output must be at least source size");
     if (!plan) return set_error(SPLAT_ERR_PARAMETER, "upscale plan required (splat_upscale_plan)");
+    // source rows are staged with 16-byte bulk copies; rows of out_w % 4 == 0 frames are
+    // written with 16-byte (bulk / vector) stores
+    if ((uintptr_t)src & 15) return set_error(SPLAT_ERR_PARAMETER, "source planes must be 16-byte aligned");
+    if ((out_w & 3) == 0 && ((uintptr_t)out & 15))
+        return set_error(SPLAT_ERR_PARAMETER, "output must be 16-byte aligned");
     return upscale_forward_impl(src, in_w, in_h, out, out_w, out_h, clamp, plan, (cudaStream_t)stream);
 }
 

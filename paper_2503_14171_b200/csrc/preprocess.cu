@@ -201,7 +201,10 @@ __global__ void pack64_kernel(SceneConst sc, ViewConst vc, double* __restrict__ 
 #define BIN_STAGE 16384
 #endif
 constexpr int kBinBlock = BIN_BLOCK;   // ranks per block (a histogram row)
-constexpr int kBinThreads = 1024;    // kBinBlock / kBinThreads ranks per thread
+#ifndef BIN_THREADS
+#define BIN_THREADS 1024
+#endif
+constexpr int kBinThreads = BIN_THREADS;   // kBinBlock / kBinThreads ranks per thread
 constexpr int kBinRPT = kBinBlock / kBinThreads;
 constexpr int kBinStage = BIN_STAGE;   // staged pairs per pass of the fill (2 CTAs/SM fit)
 constexpr int kColGroup = 16;        // rows per column-scan group

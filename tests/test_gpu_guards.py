@@ -104,3 +104,36 @@ def test_loss_writes_only_its_buffers(w, h):
     assert adj.intact() and val.intact()
     v2, a2 = fit.loss_device(pred, tgt, 0.2, slot=8)
     assert torch.equal(adj.t, a2) and torch.equal(val.t, v2)
+
+
+def test_abi_rejects_misaligned_buffers():
+    """The bulk-copy (TMA) paths need aligned buffers: the C ABI refuses a frame workspace
+    that is not 256-byte aligned and upscale planes / frames that are not 16-byte aligned
+    (status 2 = ParameterError) instead of faulting."""
+    import torch
+    import paper_2503_14171_b200 as P
+    from paper_2503_14171_b200 import _lib
+    from paper_2503_14171_b200.core import ParameterError
+    from paper_2503_14171_b200.device import to_device
+    from paper_2503_14171_b200.raster_forward import Frame, make_view
+    lib = _lib.load()
+    sc = P.synthetic_scene(500, 64, 48, (0.5, 3.0), seed=2)
+    ds = to_device(sc)
+    fr = Frame(ds.n, 64, 48, 1 << 16, torch.device("cuda"))
+    big = torch.empty(fr.nbytes + 256, dtype=torch.uint8, device="cuda")
+    v = make_view(ds, 64, 48)
+    rc = lib.splat_prepare_view(_lib.ptr(ds.const), ds.n, v, 64, 48, big.data_ptr() + 16, fr.nbytes, fr.capacity,
+                                _lib.stream_ptr())
+    assert rc == _lib.SPLAT_ERR_PARAMETER
+    with pytest.raises(ParameterError):
+        _lib.check(rc)
+    src = torch.zeros(48 * 64 * 12 + 4, device="cuda")
+    out = torch.zeros(96 * 128 * 3 + 4, device="cuda")
+    from paper_2503_14171_b200.spline import upscale_plan
+    plan = upscale_plan(64, 48, 128, 96, torch.device("cuda"))
+    assert lib.splat_upscale_forward(src.data_ptr() + 4, 64, 48, out.data_ptr(), 128, 96, 1, _lib.ptr(plan),
+                                     _lib.stream_ptr()) == _lib.SPLAT_ERR_PARAMETER
+    assert lib.splat_upscale_forward(src.data_ptr(), 64, 48, out.data_ptr() + 4, 128, 96, 1, _lib.ptr(plan),
+                                     _lib.stream_ptr()) == _lib.SPLAT_ERR_PARAMETER
+    assert lib.splat_upscale_forward(src.data_ptr(), 64, 48, out.data_ptr(), 128, 96, 1, _lib.ptr(plan),
+                                     _lib.stream_ptr()) == 0
