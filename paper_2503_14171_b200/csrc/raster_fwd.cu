@@ -290,37 +290,20 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
     if (st != kCulled) apply_candidate<TRAIN>(st, al, gax, gay, gaxy, rel, col, j, s, active, flagged);
 }
 
-// Each warp streams the tile's candidate list itself (no block barriers).  The
-// warp's 8x4 pixel rectangle is split into four 4x2 groups of 8 lanes; 32
-// candidates per step are loaded one per lane, culled against the warp
-// rectangle and then each group rectangle with the exact ellipse test, staged
-// in the warp's shared-memory slice, and compacted into one in-order list per
-// group.  Step k of the blend loop then advances every group by one of ITS
-// candidates (four candidates per warp instruction stream), which roughly
-// halves the lanes idling on candidates that miss their pixels.
-#ifndef RASTER_PACK_PAD
-#define RASTER_PACK_PAD 1
-#endif
-#ifndef RASTER_NO_WARP_EXACT
-#define RASTER_NO_WARP_EXACT 1
-#endif
-#ifndef RASTER_TERM_MASK
-#define RASTER_TERM_MASK 7
-#endif
+// Each warp streams its tile's candidate list itself (no block barriers), compacted
+// to the pairs whose bbox reaches its 8x4 rectangle (see raster_fwd_kernel).  The
+// rectangle is split into four 4x2 groups of 8 lanes; per chunk of 32 staged
+// candidates each group gets its own in-order list (extent box + Q-norm bound), and
+// step k of the blend loop advances every group by one of ITS candidates (four
+// candidates per warp instruction stream).
 #ifndef RASTER_STATS
-#define RASTER_STATS 0
-#endif
-#ifndef RASTER_GROUP_EXACT
-#define RASTER_GROUP_EXACT 0
-#endif
-#ifndef RASTER_GROUP_DIL
-#define RASTER_GROUP_DIL 1
+#define RASTER_STATS 0   // work counters for tools/raster_stats.py
 #endif
 #ifndef RASTER_MIN_BLOCKS
-#define RASTER_MIN_BLOCKS 5
+#define RASTER_MIN_BLOCKS 5   // 5 x 128 threads x 96 registers (6: spills, slower)
 #endif
 #ifndef RASTER_UNROLL
-#define RASTER_UNROLL 2
+#define RASTER_UNROLL 2   // inference blend steps per loop iteration
 #endif
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
