@@ -498,3 +498,33 @@ def test_pipeline_rejects_bad_outputs(P):
             pipe.render([None], out=bad[None])
     ok = torch.empty((64, 128, 3), device="cuda")
     assert torch.equal(P.upscale_spline(img, 2.0, out=ok), P.upscale_spline(img, 2.0))
+
+
+def test_headline_batch_sample_matches_oracle(P, oracle):
+    """Twelve views spread over the whole 1024-view C3 batch, rendered by the bench's
+    4-slot pipeline in one pass: every frame within 1e-4 / >= 60 dB of the float64 oracle,
+    and every view's contributor counts bit-exact (render_forward of the same view)."""
+    import torch
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    from paper_2503_14171_b200.scenes import CONFIGS, random_views, synthetic_scene, view_scene
+    c = CONFIGS["c3"]
+    sc = synthetic_scene(c.n, c.width, c.height, c.scale_range, seed=5)
+    batch = random_views(c.views, c.width, c.height, seed=11)
+    idx = list(range(0, c.views, c.views // 12))[:12]
+    views = [batch[i] for i in idx]
+    pipe = ViewPipeline(sc, c.width, c.height, factor=c.factor, slots=4, views_for_capacity=views)
+    out = torch.empty((len(views), c.out_h, c.out_w, 3), dtype=torch.float32, device="cuda")
+    pipe.render(views, out=out)
+    pipe.join()
+    torch.cuda.synchronize()
+    pipe.check()
+    worst = 0.0
+    for k, v in enumerate(views):
+        ref = oracle.render_forward(view_scene(sc, v), c.width, c.height)
+        got = P.render_forward(sc, c.width, c.height, view=v)
+        assert np.array_equal(got.contrib_count.cpu().numpy(), ref.contrib_count), idx[k]
+        refup = oracle.upscale_spline(ref.color, ref.d_dx, ref.d_dy, ref.d_dxdy, c.factor)
+        diff = out[k].cpu().numpy() - refup
+        worst = max(worst, float(np.abs(diff).max()))
+        assert np.abs(diff).max() < PLANE_TOL, (idx[k], np.abs(diff).max())
+        assert 10 * np.log10(1.0 / np.mean(diff ** 2)) >= 60.0, idx[k]
