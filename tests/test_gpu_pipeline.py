@@ -82,3 +82,35 @@ def test_stage_timed_pipeline_is_bitwise_the_fused_one():
     for x, y in zip(fa, fb):
         assert torch.equal(x, y)
     assert int(a.slots[0].frame.counters()[2]) > 0   # the last view did flag pixels for the fix-up
+
+
+@pytest.mark.parametrize("w,h,factor", [(1, 1, 4.0), (3, 2, 4.0), (17, 1, 2.0), (5, 33, 2.0), (16, 16, 4.0)])
+def test_pipeline_tiny_and_ragged_renders(w, h, factor):
+    """Degenerate render sizes (1 pixel, 1-pixel rows / columns, single partial tiles)
+    through the multi-slot pipeline equal the single-view API bitwise (the reference's
+    degenerate-size tests, test_raster_forward.py:289-303)."""
+    import torch
+    import paper_2503_14171_b200 as P
+    from paper_2503_14171_b200.pipeline import ViewPipeline
+    sc = P.synthetic_scene(400, max(w, 8), max(h, 8), (0.5, 3.0), seed=w * 31 + h)
+    views = P.random_views(3, max(w, 8), max(h, 8), seed=1)
+    pipe = ViewPipeline(sc, w, h, factor=factor, slots=2, views_for_capacity=views)
+    outs = pipe.render(views, keep=True)
+    pipe.join()
+    torch.cuda.synchronize()
+    for v, got in zip(views, outs):
+        assert torch.equal(got, P.upscale_spline(P.render_forward(sc, w, h, view=v), factor))
+
+
+def test_pipeline_empty_scene_renders_background():
+    """An empty scene (render_forward's early exit, raster_forward.py:162-164) through the
+    pipeline: every upscaled frame is the background."""
+    import torch
+    import paper_2503_14171_b200 as P
+    from paper_2503_14171_b200.pipeline import render_upscale_views
+    sc = P.Scene.empty(background=(0.25, 0.5, 0.75), reference_resolution=(40, 24))
+    out = render_upscale_views(sc, 40, 24, [None, None, None], factor=2.0, slots=2)
+    torch.cuda.synchronize()
+    bg = torch.tensor([0.25, 0.5, 0.75], device="cuda")
+    assert tuple(out.shape) == (3, 48, 80, 3)
+    assert torch.allclose(out, bg.expand_as(out), rtol=0, atol=1e-7)
