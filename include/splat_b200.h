@@ -160,6 +160,24 @@ int splat_rasterize(const void *scene_const, int64_t n, const splat_view_t *view
 int splat_fixup(const void *scene_const, int64_t n, const splat_view_t *view, int width, int height,
                 int train, const splat_gimg_t *out, void *workspace, size_t ws_bytes, int64_t pair_capacity,
                 void *stream);
+/* ---- view batches (the throughput path) ---------------------------------
+ * One per-view workspace set; views are assigned round-robin (view i -> slot i % nslots) and
+ * every view's prepare -> bin -> rasterize (+ fix-up) -> upscale chain is enqueued on its
+ * slot's stream, in view order, with no host synchronisation: render_forward + upscale_spline
+ * (raster_forward.py:152-187, spline.py:162-178) for a whole batch from one call (the
+ * per-view host cost is the kernel launches only).  outs[i]: (out_h, out_w, 3) float32 frame
+ * of view i; plan from splat_upscale_plan(width, height, out_w, out_h). */
+typedef struct {
+    void *workspace;        /* frame workspace (splat_frame_workspace_bytes), 256-byte aligned */
+    size_t ws_bytes;
+    int64_t pair_capacity;
+    splat_gimg_t image;     /* the slot's GradientImage buffers (state may be NULL) */
+    void *stream;
+} splat_slot_t;
+int splat_render_views(const void *scene_const, int64_t n, const splat_view_t *views, int nviews, int width,
+                       int height, const splat_slot_t *slots, int nslots, float *const *outs, int out_w,
+                       int out_h, int clamp, const void *plan);
+
 /* Exact float64 RenderPack of a view (prepare_scene means/conics/sigmas,
  * raster_forward.py:86-102), rank order: pack64 (n,6) = mx,my,a,b,c,sigma;
  * colors64 (n,3) may be NULL.  Inspection only (the rasterizer uses float32). */

@@ -46,6 +46,10 @@ class GimgT(ctypes.Structure):
     _fields_ = [("planes", P), ("alpha", P), ("count", P), ("last", P), ("state", P)]
 
 
+class SlotT(ctypes.Structure):
+    _fields_ = [("workspace", P), ("ws_bytes", SZ), ("pair_capacity", I64), ("image", GimgT), ("stream", P)]
+
+
 class FramePtrsT(ctypes.Structure):
     _fields_ = [("bboxes", P), ("touched", P), ("offsets", P), ("keys", P), ("ranks", P),
                 ("ranges", P), ("counters", P), ("fixup", P), ("pack", P)]
@@ -74,6 +78,8 @@ SIGNATURES = {
     "splat_grad_accumulate": (I32, [P, P, I64, P]),
     "splat_render_points": (I32, [P, P, P, I64, P, P, I64, ctypes.POINTER(D), P, P, P]),
     "splat_project_3d": (I32, [I64, P, P, P, P, ctypes.POINTER(CameraT), P, P, P, P, P, P]),
+    "splat_render_views": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32, ctypes.POINTER(SlotT), I32,
+                                 ctypes.POINTER(P), I32, I32, I32, P]),
     "splat_fixup": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32, ctypes.POINTER(GimgT), P, SZ, I64, P]),
     "splat_rasterize": (I32, [P, I64, ctypes.POINTER(ViewT), I32, I32, I32,
                               ctypes.POINTER(GimgT), P, SZ, I64, P]),

@@ -276,6 +276,38 @@ int splat_adam_step(double* params, const float* grads, double* m, double* v, in
     return adam_impl(params, grads, m, v, count, lr, beta1, beta2, bc1, bc2, eps, (cudaStream_t)stream);
 }
 
+int splat_render_views(const void* scene_const, int64_t n, const splat_view_t* views, int nviews, int width,
+                       int height, const splat_slot_t* slots, int nslots, float* const* outs, int out_w, int out_h,
+                       int clamp, const void* plan) {
+    int rc = check_dims(width, height);
+    if (rc) return rc;
+    if (nviews < 0 || (nviews > 0 && (!views || !slots || nslots <= 0 || !outs)))
+        return set_error(SPLAT_ERR_PARAMETER, "invalid view batch");
+    if (!plan) return set_error(SPLAT_ERR_PARAMETER, "upscale plan required (splat_upscale_plan)");
+    if (out_w < width || out_h < height) return set_error(SPLAT_ERR_SCALE, "output must be at least source size");
+    for (int k = 0; k < nslots && k < nviews; ++k) {
+        const splat_slot_t& sl = slots[k];
+        const FrameLayout L = frame_layout(n, width, height, sl.pair_capacity);
+        if (sl.ws_bytes < L.total) return set_error(SPLAT_ERR_PARAMETER, "frame workspace too small");
+        if ((uintptr_t)sl.workspace & 255) return set_error(SPLAT_ERR_PARAMETER, "frame workspace must be 256-byte aligned");
+        if ((uintptr_t)sl.image.planes & 15) return set_error(SPLAT_ERR_PARAMETER, "image planes must be 16-byte aligned");
+    }
+    const SceneConst sc = scene_const_view(scene_const, n);
+    for (int i = 0; i < nviews; ++i) {
+        const splat_slot_t& sl = slots[i % nslots];
+        const FrameLayout L = frame_layout(n, width, height, sl.pair_capacity);
+        const ViewConst vc = make_view_const(views[i]);
+        char* w = (char*)sl.workspace;
+        cudaStream_t s = (cudaStream_t)sl.stream;
+        if ((out_w & 3) == 0 && ((uintptr_t)outs[i] & 15)) return set_error(SPLAT_ERR_PARAMETER, "output must be 16-byte aligned");
+        if ((rc = launch_preprocess(sc, vc, L, w, s))) return rc;
+        if ((rc = launch_binning(L, w, 0, s))) return rc;
+        if ((rc = launch_raster_forward(sc, vc, L, w, sl.image, false, s))) return rc;
+        if ((rc = upscale_forward_impl(sl.image.planes, width, height, outs[i], out_w, out_h, clamp, plan, s))) return rc;
+    }
+    return SPLAT_OK;
+}
+
 int splat_upscale_forward(const float* src, int in_w, int in_h, float* out, int out_w, int out_h, int clamp,
                           const void* plan, void* stream) {
     if (in_w <= 0 || in_h <= 0) return set_error(SPLAT_ERR_DIMENSION, "empty source image");

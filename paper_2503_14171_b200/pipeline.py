@@ -15,6 +15,8 @@ under-sized buffer can never silently drop splats.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import _lib
@@ -40,6 +42,7 @@ class _Slot:
 
 
 class ViewPipeline:
+    BATCHED = True   # one splat_render_views call per batch (False: the per-view ABI calls)
     def __init__(self, scene, width: int, height: int, *, factor: float = 4.0, out_size=None,
                  slots: int = 1, capacity: int | None = None, views_for_capacity=None):
         self.scene = to_device(scene)
@@ -58,6 +61,13 @@ class ViewPipeline:
         self.copy_stream = None
         self.stage_events = None
         self.plan = upscale_plan(self.width, self.height, self.out_w, self.out_h, self.scene.device)
+        # the slots as the batched C entry point sees them (splat_render_views)
+        self._cslots = (_lib.SlotT * self.nslots)()
+        for k, slot in enumerate(self.slots):
+            cs = self._cslots[k]
+            cs.workspace, cs.ws_bytes, cs.pair_capacity = _lib.ptr(slot.frame.ws), slot.frame.nbytes, slot.frame.capacity
+            cs.image = slot.gimg
+            cs.stream = _lib.stream_ptr(slot.stream)
 
     # ---- capacity -------------------------------------------------------------------------
     def calibrate(self, views, margin: float = 1.05) -> int:
@@ -100,6 +110,8 @@ class ViewPipeline:
         # every slot (and the copy stream) starts after the work the caller queued so far on
         # its stream: the scene upload / prepare, the Frame counter zeroing, the upscale plan
         self.fork()
+        if self.BATCHED and host_out is None and self.stage_events is None and len(views):
+            return self._render_batched(views, keep, out)
         for i, v in enumerate(views):
             slot = self.slots[i % self.nslots]
             cv = make_view(ds, self.width, self.height, v)
@@ -156,6 +168,28 @@ class ViewPipeline:
             if keep:
                 kept.append(dst)
         return kept
+
+    def _render_batched(self, views, keep, out):
+        """The whole batch through splat_render_views: one C call enqueues every view's
+        prepare -> bin -> raster -> fix-up -> upscale chain on its slot's stream."""
+        lib, ds = self.lib, self.scene
+        n = len(views)
+        cviews = (_lib.ViewT * n)(*[make_view(ds, self.width, self.height, v) for v in views])
+        dsts = []
+        for i in range(n):
+            slot = self.slots[i % self.nslots]
+            if out is not None:
+                dsts.append(out[i])
+            elif keep:
+                dsts.append(torch.empty((self.out_h, self.out_w, 3), dtype=torch.float32, device=ds.device))
+            else:
+                dsts.append(slot.out[slot.flip])
+                slot.flip ^= 1
+        ptrs = (ctypes.c_void_p * n)(*[d.data_ptr() for d in dsts])
+        _lib.check(lib.splat_render_views(_lib.ptr(ds.const), ds.n, cviews, n, self.width, self.height,
+                                          self._cslots, self.nslots, ptrs, self.out_w, self.out_h, 1,
+                                          _lib.ptr(self.plan)))
+        return dsts if keep else None
 
     def join(self, stream=None):
         """Make `stream` (default: current) wait for all slot streams and copies."""
