@@ -485,12 +485,12 @@ def train_line(args, rank, world, local):
         sm_mhz = (clk or {}).get("sm_mhz") or 1335.0
         peak = NUM_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
         ach = flops / (tms * 1e-3) / 1e12
-        roof = {"kernel": "raster_bwd_kernel + reduce_pairs_kernel + chain_kernel (splat_render_backward, per view)",
+        roof = {"kernel": "raster_bwd2_kernel + reduce_pairs2_kernel + chain_kernel (splat_render_backward, per view)",
                 "bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                 "measured": f"CUDA events around the splat_render_backward call, {len(mine)} views one at a time",
                 "algorithmic": {"formula": "27P + 13E + 360K (SURVEY 8d backward; E = bbox-tested upper bound)",
                                 "flops_per_view": flops / len(mine)},
-                "traffic": json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("raster_bwd_kernel")
+                "traffic": json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("raster_bwd2_kernel")
                 if os.path.exists(os.path.join(ROOT, "profiles", "ncu_traffic.json")) else None,
                 "ms_per_view": tms / len(mine)}
     if rank == 0:

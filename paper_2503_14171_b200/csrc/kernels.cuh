@@ -19,7 +19,7 @@ int radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, c
 // Frame workspace layout (all offsets 256-byte aligned).
 struct FrameLayout {
     size_t bboxes, touched, offsets, scan_scratch, keys0, vals0, vals1, slot_pos, tile_scan,
-        ranges, tile_count, tile_start, cursor, big_list, bin_hist, bin_pre, bin_part, counters, fixup, pack, rmask, total;
+        ranges, tile_count, tile_start, cursor, big_list, bin_hist, bin_pre, bin_part, counters, fixup, pack, rmask, bwd_hi, bwd_cursor, total;
     int64_t n, cap;
     int width, height, ntx, nty;
 };

@@ -743,6 +743,8 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap) {
     L.fixup = o; o = align_up(o + (size_t)width * height * 4 + 4);
     L.pack = o; o = align_up(o + nn * sizeof(PackF));
     L.rmask = o; o = align_up(o + cc + kPairPad);   // per pair: rect_mask of its tile (u8)
+    L.bwd_hi = o; o = align_up(o + (size_t)L.ntx * L.nty * 8 * 4);   // backward: replay start per rectangle
+    L.bwd_cursor = o; o = align_up(o + 16);                          // backward: work-unit counter
     L.total = o;
     return L;
 }
