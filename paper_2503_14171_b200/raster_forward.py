@@ -94,7 +94,9 @@ class GradientImage:
     def from_planes(cls, color, d_dx, d_dy, d_dxdy, device=None) -> "GradientImage":
         """Pack user-provided (H, W, 3) planes (numpy or torch) into a GradientImage."""
         def t(a):
-            a = torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a)
+            if not torch.is_tensor(a):
+                a = np.asarray(a)
+                a = torch.as_tensor(a if a.flags.writeable else a.copy())
             return a.to(device=device or torch.device("cuda", torch.cuda.current_device()),
                         dtype=torch.float32)
         planes = torch.stack([t(color), t(d_dx), t(d_dy), t(d_dxdy)], dim=2).contiguous()
