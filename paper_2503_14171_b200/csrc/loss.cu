@@ -38,7 +38,36 @@ __constant__ double c_wind[11];
 // variances are differences of nearly equal second moments, and their float32
 // rounding (amplified by cancellation in the splat-gradient sums) would exceed
 // the 1e-3 gradient tolerance.  Inputs and the outputs' consumers stay float32.
-constexpr size_t kStatsSmem = 2 * (size_t)kHalo * (kHalo + 1) * 4 + 5 * (size_t)kHalo * kS * 8;
+//
+// A CTA owns a 32-column strip of one channel over kSegTiles tile rows and walks it
+// down in 32-row chunks: each image row's horizontal moments are computed once
+// (a ring of 42 rows in shared memory carries the 10 rows the next chunk's vertical
+// window shares with this one), so the horizontal pass does 32 rows of work per
+// 32 output rows instead of 42, in exactly one (row, 4 columns) item per thread;
+// the next chunk's input rows land by cp.async while this chunk computes.
+#ifndef SSIM_SEG_TILES
+#define SSIM_SEG_TILES 6
+#endif
+#ifndef SSIM_PREFETCH
+#define SSIM_PREFETCH 0   // 1: double-buffered input rows (76 KB: 2 CTAs/SM); 0: one buffer (65 KB: 3 CTAs/SM)
+#endif
+constexpr int kSegTiles = SSIM_SEG_TILES;
+constexpr int kInBufs = SSIM_PREFETCH ? 2 : 1;
+constexpr int kInStride = 45;   // = 1 mod 4: the four rows a warp's (row, 4 columns) items touch hit distinct banks
+constexpr int kRing = kS + 2 * kR;   // 42 rows of horizontal moments
+struct StatsSmem {
+    float x[kInBufs][kS][kInStride];   // input rows of the current (/ next) chunk (x: pred, y: target)
+    float y[kInBufs][kS][kInStride];
+    double hm[5][kRing][kS];         // horizontal moments, ring over image rows
+    double red[8];
+};
+constexpr size_t kStatsSmem = sizeof(StatsSmem);
+
+__device__ __forceinline__ void cp_async4_zfill(void* smem, const void* gmem, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(valid ? 4 : 0)
+                 : "memory");
+}
 
 // 1/x for x > 0: float32 reciprocal + two float64 Newton steps (~1 ulp)
 __device__ __forceinline__ double rcp64(double x) {
@@ -55,220 +84,265 @@ __global__ void __launch_bounds__(256, 3) ssim_stats_kernel(const float* __restr
                                                          double gscale, float* __restrict__ coef,
                                                          double* __restrict__ part_ssim) {
     extern __shared__ __align__(16) unsigned char sm[];
-    float(*s_x)[kHalo + 1] = reinterpret_cast<float(*)[kHalo + 1]>(sm);
-    float(*s_y)[kHalo + 1] = reinterpret_cast<float(*)[kHalo + 1]>(sm + (size_t)kHalo * (kHalo + 1) * 4);
-    double* s_h = reinterpret_cast<double*>(sm + 2 * (size_t)kHalo * (kHalo + 1) * 4);   // [5][kHalo][kS]
-    __shared__ double s_red[8];
+    StatsSmem& S = *reinterpret_cast<StatsSmem*>(sm);
     const int tid = threadIdx.x;
-    // the three channel CTAs of a tile are adjacent in launch order, so the interleaved
+    // the three channel CTAs of a strip are adjacent in launch order, so the interleaved
     // (H, W, 3) pred / target sectors one of them fetches are L2 hits for the other two
     const int ch = blockIdx.x % 3, bx = blockIdx.x / 3, gx = gridDim.x / 3;
-    const int X0 = bx * kS, Y0 = blockIdx.y * kS;
-    double local = 0.0;
-    // load the channel tile with a zero halo (zero padding: correlate1d mode="constant")
-    for (int e = tid; e < kHalo * kHalo; e += 256) {
-        const int r = e / kHalo, c = e - r * kHalo;
-        const int gy = Y0 + r - kR, gx = X0 + c - kR;
-        float xv = 0.f, yv = 0.f;
-        if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
-            const size_t o = ((size_t)gy * w + gx) * 3 + ch;
-            xv = pred[o];
-            yv = target[o];
+    const int gy = (h + kS - 1) / kS;
+    const int ty0 = blockIdx.y * kSegTiles, nchunks = min(kSegTiles, gy - ty0);
+    const int X0 = bx * kS, Yseg = ty0 * kS;
+    // input rows [gy0, gy0 + nrows) of the strip (+ halo columns), zero outside the image
+    auto load_rows = [&](int buf, int gy0, int nrows) {
+        for (int e = tid; e < nrows * kHalo; e += 256) {
+            const int r = e / kHalo, c = e - r * kHalo;
+            const int yy = gy0 + r, xx = X0 + c - kR;
+            const bool ok = yy >= 0 && yy < h && xx >= 0 && xx < w;
+            const size_t o = ok ? ((size_t)yy * w + xx) * 3 + ch : 0;
+            cp_async4_zfill(&S.x[buf][r][c], pred + o, ok);
+            cp_async4_zfill(&S.y[buf][r][c], target + o, ok);
         }
-        s_x[r][c] = xv;
-        s_y[r][c] = yv;
-    }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // horizontal moments of input rows [gy0, gy0 + nrows) (in buffer buf) into the ring
+    auto hpass = [&](int buf, int gy0, int nrows) {
+        for (int e = tid; e < nrows * (kS / 4); e += 256) {
+            const int r = e / (kS / 4), c0 = (e - r * (kS / 4)) * 4;
+            double m[4][5];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 5; ++q) m[i][q] = 0.0;
+#pragma unroll
+            for (int t = 0; t < 14; ++t) {
+                const double xv = S.x[buf][r][c0 + t], yv = S.y[buf][r][c0 + t];
+                const double xx = xv * xv, yy = yv * yv, xy = xv * yv;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int k = t - i;
+                    if (k < 0 || k > 10) continue;
+                    const double wk = c_wind[k];
+                    m[i][0] = fma(wk, xv, m[i][0]);
+                    m[i][1] = fma(wk, yv, m[i][1]);
+                    m[i][2] = fma(wk, xx, m[i][2]);
+                    m[i][3] = fma(wk, yy, m[i][3]);
+                    m[i][4] = fma(wk, xy, m[i][4]);
+                }
+            }
+            const int slot = (gy0 + r - (Yseg - kR)) % kRing;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 5; ++q) S.hm[q][slot][c0 + i] = m[i][q];
+        }
+    };
+    // the segment's top halo rows [Yseg - 5, Yseg + 5), then chunk 0's rows [Yseg + 5, Yseg + 37)
+    load_rows(kInBufs - 1, Yseg - kR, 2 * kR);
+    if (SSIM_PREFETCH) load_rows(0, Yseg + kR, kS);
+    if (SSIM_PREFETCH) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    // horizontal pass, register-blocked: one (row, 4 consecutive columns) item per thread step
-    for (int e = tid; e < kHalo * (kS / 4); e += 256) {
-        const int r = e / (kS / 4), c0 = (e - r * (kS / 4)) * 4;
-        double m[4][5];
+    hpass(kInBufs - 1, Yseg - kR, 2 * kR);
+    if (SSIM_PREFETCH) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    for (int k = 0; k < nchunks; ++k) {
+        const int y0 = Yseg + k * kS, b = SSIM_PREFETCH ? (k & 1) : 0;
+        if (SSIM_PREFETCH) {
+            if (k + 1 < nchunks) load_rows(b ^ 1, y0 + kS + kR, kS);   // buffer b^1 was read before the last barrier
+        } else {
+            load_rows(0, y0 + kR, kS);   // the buffer was read before the last barrier
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+        }
+        hpass(b, y0 + kR, kS);
+        __syncthreads();
+        // vertical pass, register-blocked: thread = (column, 4 consecutive rows) -> exactly 256 items
+        double local = 0.0;
+        {
+            const int c = tid & (kS - 1), r0 = (tid >> 5) * 4;
+            const int base = y0 + r0 - kR - (Yseg - kR);   // ring index of the window's first row
+            double m[4][5];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int q = 0; q < 5; ++q) m[i][q] = 0.0;
+                for (int q = 0; q < 5; ++q) m[i][q] = 0.0;
 #pragma unroll
-        for (int t = 0; t < 14; ++t) {
-            const double xv = s_x[r][c0 + t], yv = s_y[r][c0 + t];
-            const double xx = xv * xv, yy = yv * yv, xy = xv * yv;
+            for (int t = 0; t < 14; ++t) {
+                const int slot = (base + t) % kRing;
+                double hv[5];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) hv[q] = S.hm[q][slot][c];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int kk = t - i;
+                    if (kk < 0 || kk > 10) continue;
+                    const double wk = c_wind[kk];
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) m[i][q] = fma(wk, hv[q], m[i][q]);
+                }
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int k = t - i;
-                if (k < 0 || k > 10) continue;
-                const double wk = c_wind[k];
-                m[i][0] = fma(wk, xv, m[i][0]);
-                m[i][1] = fma(wk, yv, m[i][1]);
-                m[i][2] = fma(wk, xx, m[i][2]);
-                m[i][3] = fma(wk, yy, m[i][3]);
-                m[i][4] = fma(wk, xy, m[i][4]);
+                const int yy = y0 + r0 + i, xx = X0 + c;
+                if (yy >= h || xx >= w) continue;
+                const double ux = m[i][0], uy = m[i][1];
+                const double sxx = m[i][2] - ux * ux, syy = m[i][3] - uy * uy, sxy = m[i][4] - ux * uy;
+                const double n1 = 2.0 * ux * uy + kC1, n2 = 2.0 * sxy + kC2;
+                const double d1 = ux * ux + uy * uy + kC1, d2 = sxx + syy + kC2;
+                const bool interior = yy >= kR && yy < h - kR && xx >= kR && xx < w - kR;
+                float gux = 0.f, gvx = 0.f, gvxy = 0.f;
+                if (interior) {
+                    const double r1 = rcp64(d1), r2 = rcp64(d2);
+                    const double pq = n1 * r1, qq = n2 * r2;
+                    local += pq * qq;
+                    gux = (float)(gscale * (qq * (2.0 * uy * d1 - 2.0 * ux * n1) * (r1 * r1) +
+                                            pq * (-2.0 * uy * r2 + 2.0 * ux * n2 * (r2 * r2))));
+                    gvx = (float)(gscale * pq * (-n2 * (r2 * r2)));
+                    gvxy = (float)(gscale * pq * (2.0 * r2));
+                }
+                // planar coefficient maps [(ch * 3 + q)][H][W]: coalesced stores and loads
+                const size_t hw = (size_t)h * w, o = (size_t)yy * w + xx;
+                coef[(size_t)(ch * 3) * hw + o] = gux;
+                coef[(size_t)(ch * 3 + 1) * hw + o] = gvx;
+                coef[(size_t)(ch * 3 + 2) * hw + o] = gvxy;
             }
         }
+        // fixed-order block reduction of the chunk's (= one 32x32 tile's) SSIM map sum
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int q = 0; q < 5; ++q) s_h[((size_t)q * kHalo + r) * kS + c0 + i] = m[i][q];
-    }
-    __syncthreads();
-    // vertical pass, register-blocked: thread = (column, 4 consecutive rows) -> exactly 256 items
-    {
-        const int c = tid & (kS - 1), r0 = (tid >> 5) * 4;
-        double m[4][5];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int q = 0; q < 5; ++q) m[i][q] = 0.0;
-#pragma unroll
-        for (int t = 0; t < 14; ++t) {
-            double hv[5];
-#pragma unroll
-            for (int q = 0; q < 5; ++q) hv[q] = s_h[((size_t)q * kHalo + r0 + t) * kS + c];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int k = t - i;
-                if (k < 0 || k > 10) continue;
-                const double wk = c_wind[k];
-#pragma unroll
-                for (int q = 0; q < 5; ++q) m[i][q] = fma(wk, hv[q], m[i][q]);
-            }
+        for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
+        if ((tid & 31) == 0) S.red[tid >> 5] = local;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int i = 0; i < 8; ++i) t += S.red[i];
+            part_ssim[((size_t)ch * gy + ty0 + k) * gx + bx] = t;
         }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int gy = Y0 + r0 + i, gx = X0 + c;
-            if (gy >= h || gx >= w) continue;
-            const double ux = m[i][0], uy = m[i][1];
-            const double sxx = m[i][2] - ux * ux, syy = m[i][3] - uy * uy, sxy = m[i][4] - ux * uy;
-            const double n1 = 2.0 * ux * uy + kC1, n2 = 2.0 * sxy + kC2;
-            const double d1 = ux * ux + uy * uy + kC1, d2 = sxx + syy + kC2;
-            const bool interior = gy >= kR && gy < h - kR && gx >= kR && gx < w - kR;
-            float gux = 0.f, gvx = 0.f, gvxy = 0.f;
-            if (interior) {
-                const double r1 = rcp64(d1), r2 = rcp64(d2);
-                const double pq = n1 * r1, qq = n2 * r2;
-                local += pq * qq;
-                gux = (float)(gscale * (qq * (2.0 * uy * d1 - 2.0 * ux * n1) * (r1 * r1) +
-                                        pq * (-2.0 * uy * r2 + 2.0 * ux * n2 * (r2 * r2))));
-                gvx = (float)(gscale * pq * (-n2 * (r2 * r2)));
-                gvxy = (float)(gscale * pq * (2.0 * r2));
-            }
-            // planar coefficient maps [(ch * 3 + q)][H][W]: coalesced stores and loads
-            const size_t hw = (size_t)h * w, o = (size_t)gy * w + gx;
-            coef[(size_t)(ch * 3) * hw + o] = gux;
-            coef[(size_t)(ch * 3 + 1) * hw + o] = gvx;
-            coef[(size_t)(ch * 3 + 2) * hw + o] = gvxy;
-        }
-    }
-    // fixed-order block reduction of the SSIM map sum
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
-    if ((tid & 31) == 0) s_red[tid >> 5] = local;
-    __syncthreads();
-    if (tid == 0) {
-        double t = 0.0;
-        for (int i = 0; i < 8; ++i) t += s_red[i];
-        part_ssim[((size_t)ch * gridDim.y + blockIdx.y) * gx + bx] = t;
+        // (the next chunk's hpass overwrites ring rows this chunk's vertical pass read;
+        //  its S.red writes come after the next barrier)
+        __syncthreads();
     }
 }
+
+// The gradient filter walks the same strips: the three coefficient maps' horizontal
+// passes go to a 42-row ring, one 32-row chunk (= one output tile) at a time.
+struct GradSmem {
+    float c[3][kS][kInStride];   // coefficient-map rows of the chunk (+ halo columns)
+    float h[3][kRing][kS + 1];   // horizontal passes, ring over image rows
+    float red[8];
+};
 
 __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict__ pred,
                                                         const float* __restrict__ target, int w, int h,
                                                         const float* __restrict__ coef, float l1_scale,
                                                         float lam, float* __restrict__ adj,
                                                         float* __restrict__ part_l1) {
-    __shared__ float s_c[3][kHalo][kHalo + 1];
-    __shared__ float s_h[3][kHalo][kS + 1];
-    __shared__ float s_red[8];
+    __shared__ GradSmem S;
     const int tid = threadIdx.x;
-    // the three channel CTAs of a tile are adjacent in launch order, so the interleaved
+    // the three channel CTAs of a strip are adjacent in launch order, so the interleaved
     // (H, W, 3) pred / target sectors one of them fetches are L2 hits for the other two
     const int ch = blockIdx.x % 3, bx = blockIdx.x / 3, gx = gridDim.x / 3;
-    const int X0 = bx * kS, Y0 = blockIdx.y * kS;
-    float local = 0.f;
-    for (int e = tid; e < kHalo * kHalo; e += 256) {
-        const int r = e / kHalo, c = e - r * kHalo;
-        const int gy = Y0 + r - kR, gx = X0 + c - kR;
-        float a = 0.f, b = 0.f, d = 0.f;
-        if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
-            const size_t hw = (size_t)h * w, o = (size_t)gy * w + gx;
-            a = coef[(size_t)(ch * 3) * hw + o];
-            b = coef[(size_t)(ch * 3 + 1) * hw + o];
-            d = coef[(size_t)(ch * 3 + 2) * hw + o];
+    const int gy = (h + kS - 1) / kS;
+    const int ty0 = blockIdx.y * kSegTiles, nchunks = min(kSegTiles, gy - ty0);
+    const int X0 = bx * kS, Yseg = ty0 * kS;
+    const size_t hw = (size_t)h * w;
+    auto load_rows = [&](int gy0, int nrows) {
+        for (int e = tid; e < nrows * kHalo; e += 256) {
+            const int r = e / kHalo, c = e - r * kHalo;
+            const int yy = gy0 + r, xx = X0 + c - kR;
+            const bool ok = yy >= 0 && yy < h && xx >= 0 && xx < w;
+            const size_t o = ok ? (size_t)yy * w + xx : 0;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) cp_async4_zfill(&S.c[q][r][c], coef + (size_t)(ch * 3 + q) * hw + o, ok);
         }
-        s_c[0][r][c] = a;
-        s_c[1][r][c] = b;
-        s_c[2][r][c] = d;
-    }
-    __syncthreads();
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+    };
     // horizontal pass, register-blocked: (row, 4 consecutive columns) per item
-    for (int e = tid; e < kHalo * (kS / 4); e += 256) {
-        const int r = e / (kS / 4), c0 = (e - r * (kS / 4)) * 4;
-        float m[4][3];
+    auto hpass = [&](int gy0, int nrows) {
+        for (int e = tid; e < nrows * (kS / 4); e += 256) {
+            const int r = e / (kS / 4), c0 = (e - r * (kS / 4)) * 4;
+            float m[4][3];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int q = 0; q < 3; ++q) m[i][q] = 0.f;
+                for (int q = 0; q < 3; ++q) m[i][q] = 0.f;
 #pragma unroll
-        for (int t = 0; t < 14; ++t) {
-            float v[3];
+            for (int t = 0; t < 14; ++t) {
+                float v[3];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) v[q] = s_c[q][r][c0 + t];
+                for (int q = 0; q < 3; ++q) v[q] = S.c[q][r][c0 + t];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int k = t - i;
+                    if (k < 0 || k > 10) continue;
+                    const float wk = c_win[k];
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) m[i][q] = fmaf(wk, v[q], m[i][q]);
+                }
+            }
+            const int slot = (gy0 + r - (Yseg - kR)) % kRing;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) S.h[q][slot][c0 + i] = m[i][q];
+        }
+    };
+    load_rows(Yseg - kR, 2 * kR);   // the segment's top halo rows
+    hpass(Yseg - kR, 2 * kR);
+    __syncthreads();
+    for (int k = 0; k < nchunks; ++k) {
+        const int y0 = Yseg + k * kS;
+        load_rows(y0 + kR, kS);     // (the buffer was read before the last barrier)
+        hpass(y0 + kR, kS);
+        __syncthreads();
+        float local = 0.f;
+        {
+            const int c = tid & (kS - 1), r0 = (tid >> 5) * 4;
+            const int base = y0 + r0 - kR - (Yseg - kR);
+            float m[4][3];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) m[i][q] = 0.f;
+#pragma unroll
+            for (int t = 0; t < 14; ++t) {
+                const int slot = (base + t) % kRing;
+                float v[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) v[q] = S.h[q][slot][c];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int kk = t - i;
+                    if (kk < 0 || kk > 10) continue;
+                    const float wk = c_win[kk];
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) m[i][q] = fmaf(wk, v[q], m[i][q]);
+                }
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int k = t - i;
-                if (k < 0 || k > 10) continue;
-                const float wk = c_win[k];
-#pragma unroll
-                for (int q = 0; q < 3; ++q) m[i][q] = fmaf(wk, v[q], m[i][q]);
+                const int yy = y0 + r0 + i, xx = X0 + c;
+                if (yy >= h || xx >= w) continue;
+                const size_t o = ((size_t)yy * w + xx) * 3 + ch;
+                const float x = pred[o], y = target[o];
+                const float dssim = m[i][0] + 2.f * x * m[i][1] + y * m[i][2];
+                const float diff = x - y;
+                const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
+                adj[o] = l1_scale * sgn - lam * dssim;
+                local += fabsf(diff);
             }
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int q = 0; q < 3; ++q) s_h[q][r][c0 + i] = m[i][q];
-    }
-    __syncthreads();
-    // vertical pass, register-blocked: (column, 4 consecutive rows) per thread
-    {
-        const int c = tid & (kS - 1), r0 = (tid >> 5) * 4;
-        float m[4][3];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int q = 0; q < 3; ++q) m[i][q] = 0.f;
-#pragma unroll
-        for (int t = 0; t < 14; ++t) {
-            float v[3];
-#pragma unroll
-            for (int q = 0; q < 3; ++q) v[q] = s_h[q][r0 + t][c];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int k = t - i;
-                if (k < 0 || k > 10) continue;
-                const float wk = c_win[k];
-#pragma unroll
-                for (int q = 0; q < 3; ++q) m[i][q] = fmaf(wk, v[q], m[i][q]);
-            }
+        for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
+        if ((tid & 31) == 0) S.red[tid >> 5] = local;
+        __syncthreads();
+        if (tid == 0) {
+            float t = 0.f;
+            for (int i = 0; i < 8; ++i) t += S.red[i];
+            part_l1[((size_t)ch * gy + ty0 + k) * gx + bx] = t;
         }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int gy = Y0 + r0 + i, gx = X0 + c;
-            if (gy >= h || gx >= w) continue;
-            const size_t o = ((size_t)gy * w + gx) * 3 + ch;
-            const float x = pred[o], y = target[o];
-            const float dssim = m[i][0] + 2.f * x * m[i][1] + y * m[i][2];
-            const float diff = x - y;
-            const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
-            adj[o] = l1_scale * sgn - lam * dssim;
-            local += fabsf(diff);
-        }
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
-    if ((tid & 31) == 0) s_red[tid >> 5] = local;
-    __syncthreads();
-    if (tid == 0) {
-        float t = 0.f;
-        for (int i = 0; i < 8; ++i) t += s_red[i];
-        part_l1[((size_t)ch * gridDim.y + blockIdx.y) * gx + bx] = t;
     }
 }
 
@@ -389,14 +463,14 @@ int loss_impl(const float* pred, const float* target, int w, int h, double lam, 
     const double inner = (double)(h - 2 * kR) * (double)(w - 2 * kR);
     const double size = (double)w * h * 3;
     const double gscale = 1.0 / (inner * 3.0);
-    dim3 grid(3 * gx, gy);   // channel fastest (see ssim_stats_kernel)
-    if (lam > 0.0) {
-        ssim_stats_kernel<<<grid, 256, kStatsSmem, stream>>>(pred, target, w, h, gscale, coef, part_ssim); note_launch();
+    if (lam > 0.0) {   // grids: channel fastest (see ssim_stats_kernel)
+        const dim3 sgrid(3 * gx, ceil_div(gy, kSegTiles));
+        ssim_stats_kernel<<<sgrid, 256, kStatsSmem, stream>>>(pred, target, w, h, gscale, coef, part_ssim); note_launch();
     } else {
         SPLAT_CUDA_CHECK(cudaMemsetAsync(coef, 0, (size_t)w * h * 9 * 4, stream));
         SPLAT_CUDA_CHECK(cudaMemsetAsync(part_ssim, 0, nparts * 3 * 8, stream));
     }
-    ssim_grad_kernel<<<grid, 256, 0, stream>>>(pred, target, w, h, coef, (float)((1.0 - lam) / size), (float)lam,
+    ssim_grad_kernel<<<dim3(3 * gx, ceil_div(gy, kSegTiles)), 256, 0, stream>>>(pred, target, w, h, coef, (float)((1.0 - lam) / size), (float)lam,
                                                adj, part_l1); note_launch();
     loss_finish_kernel<<<1, 768, 0, stream>>>(part_ssim, part_l1, (int)nparts, size, inner, lam, value);
     note_launch();

@@ -28,6 +28,24 @@ def test_loss_matches_reference(P):
         assert err < 1e-4, (lam, err)
 
 
+@pytest.mark.parametrize("h,w", [(453, 200), (1080, 1920), (37, 70)])
+def test_loss_matches_oracle_ragged(P, oracle, h, w):
+    """The SSIM statistics walk 32-column strips in 32-row chunks over segments of tile
+    rows: ragged strips, partial last chunks, several segments and a single-chunk image
+    all give the oracle's value (1e-6 relative) and adjoint (1e-4 of its max, as the
+    golden test: the coefficient maps and their filtering are float32)."""
+    from paper_2503_14171_b200 import fit
+    rng = np.random.default_rng(h * w)
+    pred = rng.random((h, w, 3)).astype(np.float32)
+    tgt = np.clip(pred + 0.05 * rng.standard_normal((h, w, 3)), 0, 1).astype(np.float32)
+    pred[h // 3:h // 2, : w // 2] = 0.25          # flat patches: variances near the C2 floor
+    tgt[h // 3:h // 2, : w // 2] = 0.25
+    value, adj = fit.loss(pred, tgt, 0.2)
+    rv, radj = oracle.loss(pred.astype(np.float64), tgt.astype(np.float64), 0.2)
+    assert abs(value - rv) <= 1e-6 * abs(rv), (value, rv)
+    assert np.abs(adj.double().cpu().numpy() - radj).max() <= 1e-4 * np.abs(radj).max()
+
+
 def test_loss_validation(P):
     from paper_2503_14171_b200 import fit
     from paper_2503_14171_b200.core import DimensionError
