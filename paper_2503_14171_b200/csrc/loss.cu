@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256, 3) ssim_stats_kernel(const float* __restr
 // The gradient filter walks the same strips: the three coefficient maps' horizontal
 // passes go to a 42-row ring, one 32-row chunk (= one output tile) at a time.
 struct GradSmem {
-    float c[3][kS][kInStride];   // coefficient-map rows of the chunk (+ halo columns)
+    float c[2][3][kS][kInStride];   // coefficient-map rows of the current / next chunk (+ halo columns)
     float h[3][kRing][kS + 1];   // horizontal passes, ring over image rows
     float red[8];
 };
@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
                                                         const float* __restrict__ coef, float l1_scale,
                                                         float lam, float* __restrict__ adj,
                                                         float* __restrict__ part_l1) {
-    __shared__ GradSmem S;
+    extern __shared__ __align__(16) unsigned char gsm[];
+    GradSmem& S = *reinterpret_cast<GradSmem*>(gsm);
     const int tid = threadIdx.x;
     // the three channel CTAs of a strip are adjacent in launch order, so the interleaved
     // (H, W, 3) pred / target sectors one of them fetches are L2 hits for the other two
@@ -246,21 +247,20 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
     const int ty0 = blockIdx.y * kSegTiles, nchunks = min(kSegTiles, gy - ty0);
     const int X0 = bx * kS, Yseg = ty0 * kS;
     const size_t hw = (size_t)h * w;
-    auto load_rows = [&](int gy0, int nrows) {
+    auto load_rows = [&](int buf, int gy0, int nrows) {
         for (int e = tid; e < nrows * kHalo; e += 256) {
             const int r = e / kHalo, c = e - r * kHalo;
             const int yy = gy0 + r, xx = X0 + c - kR;
             const bool ok = yy >= 0 && yy < h && xx >= 0 && xx < w;
             const size_t o = ok ? (size_t)yy * w + xx : 0;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) cp_async4_zfill(&S.c[q][r][c], coef + (size_t)(ch * 3 + q) * hw + o, ok);
+            for (int q = 0; q < 3; ++q)
+                cp_async4_zfill(&S.c[buf][q][r][c], coef + (size_t)(ch * 3 + q) * hw + o, ok);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
     };
     // horizontal pass, register-blocked: (row, 4 consecutive columns) per item
-    auto hpass = [&](int gy0, int nrows) {
+    auto hpass = [&](int buf, int gy0, int nrows) {
         for (int e = tid; e < nrows * (kS / 4); e += 256) {
             const int r = e / (kS / 4), c0 = (e - r * (kS / 4)) * 4;
             float m[4][3];
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
             for (int t = 0; t < 14; ++t) {
                 float v[3];
 #pragma unroll
-                for (int q = 0; q < 3; ++q) v[q] = S.c[q][r][c0 + t];
+                for (int q = 0; q < 3; ++q) v[q] = S.c[buf][q][r][c0 + t];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int k = t - i;
@@ -289,17 +289,31 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
                 for (int q = 0; q < 3; ++q) S.h[q][slot][c0 + i] = m[i][q];
         }
     };
-    load_rows(Yseg - kR, 2 * kR);   // the segment's top halo rows
-    hpass(Yseg - kR, 2 * kR);
+    load_rows(1, Yseg - kR, 2 * kR);   // the segment's top halo rows, then chunk 0's rows
+    load_rows(0, Yseg + kR, kS);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    hpass(1, Yseg - kR, 2 * kR);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     for (int k = 0; k < nchunks; ++k) {
-        const int y0 = Yseg + k * kS;
-        load_rows(y0 + kR, kS);     // (the buffer was read before the last barrier)
-        hpass(y0 + kR, kS);
+        const int y0 = Yseg + k * kS, b = k & 1;
+        if (k + 1 < nchunks) load_rows(b ^ 1, y0 + kS + kR, kS);   // buffer b^1 was read before the last barrier
+        // this thread's output pixels' pred / target, loaded before the filter passes
+        const int c = tid & (kS - 1), r0 = (tid >> 5) * 4;
+        float px[4], py[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int yy = y0 + r0 + i, xx = X0 + c;
+            const bool ok = yy < h && xx < w;
+            const size_t o = ok ? ((size_t)yy * w + xx) * 3 + ch : 0;
+            px[i] = ok ? pred[o] : 0.f;
+            py[i] = ok ? target[o] : 0.f;
+        }
+        hpass(b, y0 + kR, kS);
         __syncthreads();
         float local = 0.f;
         {
-            const int c = tid & (kS - 1), r0 = (tid >> 5) * 4;
             const int base = y0 + r0 - kR - (Yseg - kR);
             float m[4][3];
 #pragma unroll
@@ -326,7 +340,7 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
                 const int yy = y0 + r0 + i, xx = X0 + c;
                 if (yy >= h || xx >= w) continue;
                 const size_t o = ((size_t)yy * w + xx) * 3 + ch;
-                const float x = pred[o], y = target[o];
+                const float x = px[i], y = py[i];
                 const float dssim = m[i][0] + 2.f * x * m[i][1] + y * m[i][2];
                 const float diff = x - y;
                 const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);
@@ -337,6 +351,7 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
         if ((tid & 31) == 0) S.red[tid >> 5] = local;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
         if (tid == 0) {
             float t = 0.f;
@@ -451,6 +466,8 @@ int loss_impl(const float* pred, const float* target, int w, int h, double lam, 
         SPLAT_CUDA_CHECK(cudaMemcpyToSymbol(c_wind, wd, sizeof(wd)));
         SPLAT_CUDA_CHECK(cudaFuncSetAttribute(ssim_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)kStatsSmem));
+        SPLAT_CUDA_CHECK(cudaFuncSetAttribute(ssim_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sizeof(GradSmem)));
         v = true;
         return SPLAT_OK;
     });
@@ -470,7 +487,7 @@ int loss_impl(const float* pred, const float* target, int w, int h, double lam, 
         SPLAT_CUDA_CHECK(cudaMemsetAsync(coef, 0, (size_t)w * h * 9 * 4, stream));
         SPLAT_CUDA_CHECK(cudaMemsetAsync(part_ssim, 0, nparts * 3 * 8, stream));
     }
-    ssim_grad_kernel<<<dim3(3 * gx, ceil_div(gy, kSegTiles)), 256, 0, stream>>>(pred, target, w, h, coef, (float)((1.0 - lam) / size), (float)lam,
+    ssim_grad_kernel<<<dim3(3 * gx, ceil_div(gy, kSegTiles)), 256, sizeof(GradSmem), stream>>>(pred, target, w, h, coef, (float)((1.0 - lam) / size), (float)lam,
                                                adj, part_l1); note_launch();
     loss_finish_kernel<<<1, 768, 0, stream>>>(part_ssim, part_l1, (int)nparts, size, inner, lam, value);
     note_launch();
