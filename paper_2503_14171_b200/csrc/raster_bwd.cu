@@ -526,10 +526,14 @@ __global__ void chain_kernel(int64_t n, const int32_t* __restrict__ rank_of, con
 #ifndef BW2_WARPS
 #define BW2_WARPS 4
 #endif
+#ifndef BW2_UNROLL
+#define BW2_UNROLL 1   // candidate steps per loop iteration
+#endif
 #ifndef BW2_MIN_BLOCKS
 #define BW2_MIN_BLOCKS 4
 #endif
 constexpr int kBw2Warps = BW2_WARPS;
+constexpr int kBw2Unroll = BW2_UNROLL;
 constexpr int kBw2Threads = 32 * kBw2Warps;
 constexpr int kBw2Batch = 128;
 constexpr int kBw2Queue = 256;
@@ -759,6 +763,7 @@ __global__ void __launch_bounds__(kBw2Threads, BW2_MIN_BLOCKS) raster_bwd2_kerne
                     if (qq == q) my_mask = mq;
                 }
                 uint32_t tmask = 0;   // this lane's group: candidates it produced partials for
+#pragma unroll kBw2Unroll
                 for (int k = 0; k < cnt_max; ++k) {   // chunk index ascending = list position descending
                     const bool has = my_mask != 0u;
                     const int idx = has ? __ffs(my_mask) - 1 : 0;

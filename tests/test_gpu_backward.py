@@ -191,3 +191,53 @@ def test_training_step_gradients_match_oracle_c5_full_size(P, oracle):
         err = rel_err(grads[f], ref[f])
         assert err < 1e-3, (f, err)
         assert strict[f] >= 0.999, (f, strict[f])
+
+
+def _deep_scene(n, w, h, seed):
+    """Many faint (opacity 0.01), wide splats: every pixel blends ~900 contributors
+    before terminating, so the backward replays each pixel across dozens of 128-pair
+    windows and ring refills, from a different list position per rectangle."""
+    from paper_2503_14171_b200.core import Scene
+    rng = np.random.default_rng(seed)
+    s = rng.uniform(0.15, 0.6, (n, 2)) * min(w, h)
+    return Scene(rng.uniform(-0.1, 1.1, (n, 2)) * (w, h), np.log(s), rng.uniform(-np.pi, np.pi, n),
+                 np.full(n, np.log(0.01 / 0.99)) + rng.normal(0, 0.1, n), rng.uniform(0, 1, (n, 3)),
+                 rng.uniform(0, 1, n), np.array([0.1, 0.2, 0.3]), (w, h))
+
+
+def _check_backward_vs_oracle(P, oracle, sc, w, h, seed, label):
+    rng = np.random.default_rng(seed)
+    adjs = [rng.normal(0, 1e-3, (h, w, 3)) for _ in range(4)]
+    img = P.render_forward(sc, w, h, train=True)
+    grads = P.render_backward(sc, img, P.PixelAdjoint.of(*adjs)).numpy()
+    ref_img = oracle.render_forward(sc, w, h)
+    assert np.array_equal(img.numpy()["contrib_count"], ref_img.contrib_count), label
+    ref = oracle.render_backward(sc, ref_img, adjs)
+    for f in FIELDS:
+        err = rel_err(grads[f], ref[f])
+        assert err < 1e-3, (label, f, err)
+        assert strict_pass_fraction(grads[f], ref[f]) >= 0.999, (label, f)
+    return img
+
+
+@pytest.mark.parametrize("w,h", [(48, 40), (37, 23)])
+def test_backward_deep_replays(P, oracle, w, h):
+    img = _check_backward_vs_oracle(P, oracle, _deep_scene(3000, w, h, seed=w), w, h, 1, f"deep{w}x{h}")
+    assert int(img.numpy()["contrib_count"].max()) > 500
+
+
+def test_backward_long_tile_lists(P, oracle):
+    """Tile lists longer than 8192 pairs of which each rectangle replays only a short
+    prefix (the pixels terminate after <100 contributors): the per-rectangle replay
+    starts and the reduction's position test at work."""
+    from paper_2503_14171_b200.scenes import synthetic_scene
+    sc = synthetic_scene(70000, 40, 24, (0.3, 6.0), seed=11)
+    _check_backward_vs_oracle(P, oracle, sc, 40, 24, 2, "long-lists")
+
+
+@pytest.mark.parametrize("seed,clamped", [(0, False), (2, True)])
+def test_backward_termination_boundary_stress(P, oracle, seed, clamped):
+    """The forward's termination-boundary stress scenes (pixels deferred to the exact
+    fix-up, clamped terminators): the backward replays the same contributor sets."""
+    from test_gpu_forward import _shell_scene
+    _check_backward_vs_oracle(P, oracle, _shell_scene(seed, 160, 9, clamped), 160, 160, 3, f"shell{seed}")

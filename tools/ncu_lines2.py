@@ -7,7 +7,9 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 50
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+import os
+kf = os.environ.get("NCU_KERNEL")
+out = subprocess.run(["ncu", "-i", rep] + (["-k", "regex:" + kf] if kf else []) + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 fname, hdr, res = None, None, []
 for row in csv.reader(io.StringIO(out)):
