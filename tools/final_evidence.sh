@@ -16,5 +16,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --
 for k in raster_fwd_kernel fixup_kernel fill_rows_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 -o $O/ncu_$k $CMD > /dev/null 2>&1; echo "ncu $k rc=$?"
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ssim_stats|ssim_grad" -s 8 -c 2 \
-    -o $O/ncu_ssim python tools/kprof_train.py 1 1 1 > /dev/null 2>&1; echo "ncu ssim rc=$?"
+for k in raster_bwd2_kernel reduce_pairs2_kernel ssim_stats_kernel ssim_grad_kernel; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 6 -c 1 -o $O/ncu_$k \
+    python bench.py --workload train --steps 1 --warmup 3 --no-cpu-baseline --train-streams 1 > /dev/null 2>&1; echo "ncu $k rc=$?"
+done
