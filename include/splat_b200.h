@@ -232,6 +232,11 @@ int splat_loss(const float *pred, const float *target, int width, int height, do
  * moments, float32 gradients; bc1/bc2 = 1 - beta^t computed by the caller. */
 int splat_adam_step(double *params, const float *grads, double *m, double *v, int64_t count, double lr,
                     double beta1, double beta2, double bc1, double bc2, double eps, void *stream);
+/* The same step over up to 8 groups in one launch (fit.py:144-160's loop over groups):
+ * group k = (params[k], grads[k], m[k], v[k], counts[k] elements, lrs[k]). */
+int splat_adam_step_groups(int ngroups, double *const *params, const float *const *grads, double *const *m,
+                           double *const *v, const int64_t *counts, const double *lrs, double beta1, double beta2,
+                           double bc1, double bc2, double eps, void *stream);
 
 /* 3D EWA front-end: n 3D Gaussians (means (n,3), log_scales
  * (n,3), quaternions (n,4) w,x,y,z, opacity logits (n)) seen by `camera` ->

@@ -93,6 +93,7 @@ SIGNATURES = {
     "splat_loss_workspace_bytes": (SZ, [I32, I32]),
     "splat_loss": (I32, [P, P, I32, I32, D, P, P, P, SZ, P]),
     "splat_adam_step": (I32, [P, P, P, P, I64, D, D, D, D, D, D, P]),
+    "splat_adam_step_groups": (I32, [I32, P, P, P, P, P, P, D, D, D, D, D, P]),
     "splat_upscale_plan_bytes": (SZ, [I32, I32, I32, I32]),
     "splat_upscale_plan": (I32, [I32, I32, I32, I32, P, P]),
     "splat_upscale_forward": (I32, [P, I32, I32, P, I32, I32, I32, P, P]),

@@ -40,6 +40,9 @@ size_t backward_workspace_bytes_impl(int64_t n, int64_t cap);
 size_t loss_workspace_bytes_impl(int w, int h);
 int loss_impl(const float* pred, const float* target, int w, int h, double lam, float* adj, double* value,
               void* ws, cudaStream_t stream);
+int adam_groups_impl(int ngroups, double* const* p, const float* const* g, double* const* m, double* const* v,
+                     const int64_t* count, const double* lr, double b1, double b2, double bc1, double bc2, double eps,
+                     cudaStream_t stream);
 int adam_impl(double* p, const float* g, double* m, double* v, int64_t count, double lr, double b1, double b2,
               double bc1, double bc2, double eps, cudaStream_t stream);
 int launch_raster_backward(const SceneConst& sc, const splat_scene_t& scene, const ViewConst& vc,
@@ -274,6 +277,14 @@ int splat_loss(const float* pred, const float* target, int width, int height, do
 int splat_adam_step(double* params, const float* grads, double* m, double* v, int64_t count, double lr,
                     double beta1, double beta2, double bc1, double bc2, double eps, void* stream) {
     return adam_impl(params, grads, m, v, count, lr, beta1, beta2, bc1, bc2, eps, (cudaStream_t)stream);
+}
+
+int splat_adam_step_groups(int ngroups, double* const* params, const float* const* grads, double* const* m,
+                           double* const* v, const int64_t* counts, const double* lrs, double beta1, double beta2,
+                           double bc1, double bc2, double eps, void* stream) {
+    if (!params || !grads || !m || !v || !counts || !lrs) return set_error(SPLAT_ERR_PARAMETER, "null group arrays");
+    return adam_groups_impl(ngroups, params, grads, m, v, counts, lrs, beta1, beta2, bc1, bc2, eps,
+                            (cudaStream_t)stream);
 }
 
 int splat_render_views(const void* scene_const, int64_t n, const splat_view_t* views, int nviews, int width,

@@ -415,6 +415,60 @@ __global__ void adam_kernel(double* __restrict__ p, const float* __restrict__ g,
     p[i] = p[i] - lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
 }
 
+// All parameter groups of one step in one launch: a block-range per group (blocks of
+// 256 threads x 2 elements), the pair of elements loaded as double2 / float2 where
+// aligned.  Same per-element arithmetic as adam_kernel.
+constexpr int kAdamMaxGroups = 8;
+struct AdamGroups {
+    double* p[kAdamMaxGroups];
+    const float* g[kAdamMaxGroups];
+    double* m[kAdamMaxGroups];
+    double* v[kAdamMaxGroups];
+    int64_t count[kAdamMaxGroups];
+    double lr[kAdamMaxGroups];
+    int64_t block0[kAdamMaxGroups + 1];   // first block of each group
+    int ngroups;
+};
+
+__device__ __forceinline__ void adam_one(double& p, double& m, double& v, float g, double lr, double b1, double b2,
+                                         double bc1, double bc2, double eps) {
+    const double gi = (double)g;
+    const double mi = b1 * m + (1.0 - b1) * gi;
+    const double vi = b2 * v + (1.0 - b2) * gi * gi;
+    m = mi;
+    v = vi;
+    p = p - lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
+}
+
+__global__ void __launch_bounds__(256) adam_groups_kernel(AdamGroups a, double b1, double b2, double bc1,
+                                                          double bc2, double eps) {
+    int k = 0;
+    while (k + 1 < a.ngroups && (int64_t)blockIdx.x >= a.block0[k + 1]) ++k;
+    const int64_t i = (((int64_t)blockIdx.x - a.block0[k]) * 256 + threadIdx.x) * 2;
+    const int64_t n = a.count[k];
+    if (i >= n) return;
+    double* p = a.p[k] + i;
+    double* m = a.m[k] + i;
+    double* v = a.v[k] + i;
+    const float* g = a.g[k] + i;
+    const double lr = a.lr[k];
+    const bool vec = i + 1 < n && ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(m) |
+                                    reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(g) & 7) == 0;
+    if (vec) {
+        double2 pp = *reinterpret_cast<double2*>(p), mm = *reinterpret_cast<double2*>(m),
+                vv = *reinterpret_cast<double2*>(v);
+        const float2 gg = *reinterpret_cast<const float2*>(g);
+        adam_one(pp.x, mm.x, vv.x, gg.x, lr, b1, b2, bc1, bc2, eps);
+        adam_one(pp.y, mm.y, vv.y, gg.y, lr, b1, b2, bc1, bc2, eps);
+        *reinterpret_cast<double2*>(p) = pp;
+        *reinterpret_cast<double2*>(m) = mm;
+        *reinterpret_cast<double2*>(v) = vv;
+    } else {
+        for (int64_t j = 0; j < 2 && i + j < n; ++j) adam_one(p[j], m[j], v[j], g[j], lr, b1, b2, bc1, bc2, eps);
+    }
+}
+
 // dst += src (float32): folds per-stream gradient buffers into one, in a fixed order.
 __global__ void accumulate_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t n) {
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -491,6 +545,31 @@ int loss_impl(const float* pred, const float* target, int w, int h, double lam, 
                                                adj, part_l1); note_launch();
     loss_finish_kernel<<<1, 768, 0, stream>>>(part_ssim, part_l1, (int)nparts, size, inner, lam, value);
     note_launch();
+    SPLAT_CUDA_CHECK(cudaGetLastError());
+    return SPLAT_OK;
+}
+
+int adam_groups_impl(int ngroups, double* const* p, const float* const* g, double* const* m, double* const* v,
+                     const int64_t* count, const double* lr, double b1, double b2, double bc1, double bc2, double eps,
+                     cudaStream_t stream) {
+    if (ngroups < 0 || ngroups > kAdamMaxGroups) return set_error(SPLAT_ERR_PARAMETER, "0..8 parameter groups");
+    AdamGroups a{};
+    a.ngroups = ngroups;
+    int64_t blocks = 0;
+    for (int k = 0; k < ngroups; ++k) {
+        if (count[k] < 0) return set_error(SPLAT_ERR_PARAMETER, "negative group size");
+        a.p[k] = p[k];
+        a.g[k] = g[k];
+        a.m[k] = m[k];
+        a.v[k] = v[k];
+        a.count[k] = count[k];
+        a.lr[k] = lr[k];
+        a.block0[k] = blocks;
+        blocks += (count[k] + 511) / 512;
+    }
+    a.block0[ngroups] = blocks;
+    if (blocks == 0) return SPLAT_OK;
+    adam_groups_kernel<<<(unsigned)blocks, 256, 0, stream>>>(a, b1, b2, bc1, bc2, eps); note_launch();
     SPLAT_CUDA_CHECK(cudaGetLastError());
     return SPLAT_OK;
 }

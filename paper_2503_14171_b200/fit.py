@@ -18,6 +18,8 @@ libsplat_b200.so; torch provides the buffers, streams and the collective.
 
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -104,13 +106,22 @@ def adam_step(params: dict, grads: dict, state: AdamState, lrs: dict, beta1: flo
     bc1 = 1.0 - beta1 ** state.t
     bc2 = 1.0 - beta2 ** state.t
     st = _lib.stream_ptr()
-    for k, p in params.items():
+    keys = list(params)
+    gs = []
+    for k in keys:
         g = grads[k]
-        if tuple(g.shape) != tuple(p.shape):
+        if tuple(g.shape) != tuple(params[k].shape):
             raise DimensionError(f"gradient shape mismatch for group {k}")
-        g = g.to(dtype=torch.float32).contiguous()
-        _lib.check(lib.splat_adam_step(_lib.ptr(p), _lib.ptr(g), _lib.ptr(state.m[k]), _lib.ptr(state.v[k]),
-                                       p.numel(), float(lrs[k]), beta1, beta2, bc1, bc2, eps, st))
+        gs.append(g.to(dtype=torch.float32).contiguous())
+    # every group in one launch (splat_adam_step_groups); the per-group entry point is the same arithmetic
+    for i in range(0, len(keys), 8):
+        ks = keys[i:i + 8]
+        ng = len(ks)
+        arr = lambda xs: (ctypes.c_void_p * ng)(*[_lib.ptr(x) for x in xs])
+        _lib.check(lib.splat_adam_step_groups(
+            ng, arr([params[k] for k in ks]), arr(gs[i:i + ng]), arr([state.m[k] for k in ks]),
+            arr([state.v[k] for k in ks]), (ctypes.c_int64 * ng)(*[params[k].numel() for k in ks]),
+            (ctypes.c_double * ng)(*[float(lrs[k]) for k in ks]), beta1, beta2, bc1, bc2, eps, st))
     return params, state
 
 
