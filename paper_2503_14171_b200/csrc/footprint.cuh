@@ -126,8 +126,8 @@ __device__ __forceinline__ int eval_fast(const PackF& g, float cx, float cy, flo
     // |al - alpha_ref| / al <= 2^-21 s (Q) + 2^-20 (exp2 approx 2^-22; rounding of the
     // argument, of log2(e) and of log2(sigma), each <= 2^-22 absolute for |argument| <= 8);
     // + 2^-24 for the extra rounding of t al in the forward's T' = T - t al
+    if (lo > g.cull_hi) return kCulled;   // (rel after the cull test: culls are half the evaluations)
     rel = fmaf(s, 4.7683716e-07f, 1.0132790e-06f);
-    if (lo > g.cull_hi) return kCulled;
     if (hi >= g.cull_lo) return kUnsure;
     if (lo <= g.clamp_hi) {
         if (hi < g.clamp_lo) {
