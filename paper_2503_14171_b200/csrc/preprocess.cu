@@ -739,7 +739,7 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap) {
         L.bin_part = o; o = align_up(o + groups * L.ntx * L.nty * 4);
     }
     L.big_list = o; o = align_up(o + (size_t)L.ntx * L.nty * 4);
-    L.counters = o; o = align_up(o + 16 * 4);
+    L.counters = o; o = align_up(o + 32 * 4);   // [16..] only in RASTER_STATS builds
     L.fixup = o; o = align_up(o + (size_t)width * height * 4 + 4);
     L.pack = o; o = align_up(o + nn * sizeof(PackF));
     L.rmask = o; o = align_up(o + cc + kPairPad);   // per pair: rect_mask of its tile (u8)

@@ -523,10 +523,9 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
 #if RASTER_STATS
-                        {
-                            const uint32_t ev = __ballot_sync(0xffffffffu, active && my_mask != 0u);
-                            if (lane == 0) atomicAdd((unsigned long long*)&p.counters[14], (unsigned long long)__popc(ev));
-                        }
+                        const uint32_t ev = __ballot_sync(0xffffffffu, active && my_mask != 0u);
+                        if (lane == 0) atomicAdd((unsigned long long*)&p.counters[14], (unsigned long long)__popc(ev));
+                        const int n_before = s.n;
 #endif
                         if (active && my_mask != 0u) {
                             const int idx = __ffs(my_mask) - 1;
@@ -536,6 +535,13 @@ __global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_
                                                    &s_rank[warp][b][idx], TRAIN ? s_pos[warp][TRAIN ? b : 0][idx] : 0u,
                                                    cx, cy, s, active, flagged);
                         }
+#if RASTER_STATS   // steps in which some lane evaluated but none contributed (counters[16..17] as u64)
+                        {
+                            const uint32_t con = __ballot_sync(0xffffffffu, s.n != n_before);
+                            if (lane == 0 && ev != 0u && con == 0u) atomicAdd((unsigned long long*)&p.counters[16], 1ull);
+                            if (lane == 0 && ev != 0u) atomicAdd((unsigned long long*)&p.counters[18], (unsigned long long)__popc(con));
+                        }
+#endif
                     }
                     if (((k + kU) & 7) == 0 && !__any_sync(0xffffffffu, active)) break;
                 }

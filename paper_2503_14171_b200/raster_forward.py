@@ -175,7 +175,7 @@ class Frame:
         return ((self.width + TILE - 1) // TILE) * ((self.height + TILE - 1) // TILE)
 
     def counters(self) -> torch.Tensor:
-        return self._view(self.ptrs.counters, 16, torch.int32, (16,))
+        return self._view(self.ptrs.counters, 32, torch.int32, (32,))
 
     def bboxes(self) -> torch.Tensor:
         return self._view(self.ptrs.bboxes, 4 * max(self.n, 1), torch.int16, (max(self.n, 1), 4))[:self.n]

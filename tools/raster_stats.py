@@ -15,9 +15,11 @@ ctr[8:].zero_()
 img = P.render_forward(sc, c.width, c.height, view=v, out=img, sync_check=False)
 torch.cuda.synchronize()
 ctr = img.frame.counters().cpu().numpy().view("uint64")
-chunks, steps, entries, evals = (int(x) for x in ctr[4:8])
+chunks, steps, entries, evals, dead, conlanes = (int(x) for x in ctr[4:10])
 K = int(img.contrib_count.sum(dtype=torch.int64))
 print(f"chunks {chunks}  steps {steps} ({steps / chunks:.2f}/chunk)  group entries {entries} "
       f"({entries / max(steps, 1):.2f} of 4 groups busy per step)")
 print(f"lane-steps {steps * 32}  lane evals {evals} ({evals / (steps * 32):.1%} of lane-steps)  "
       f"contributors K {K} ({K / evals:.1%} of evals, {K / (steps * 32):.1%} of lane-steps)")
+print(f"steps with evaluations but no contributor: {dead} ({dead / max(steps, 1):.1%} of steps); "
+      f"contributing lanes per live step {conlanes / max(steps - dead, 1):.1f}")
