@@ -43,6 +43,14 @@ def test_python_binding_matches_header(lib):
     assert sorted(_lib.SIGNATURES) == declared_functions()
 
 
+def test_integration_table_names_every_entry_point():
+    """INTEGRATION.md's binding table maps every declared entry point to the reference
+    interface it replaces."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    missing = [f for f in declared_functions() if f"`{f}`" not in doc]
+    assert not missing, missing
+
+
 def test_abi_version_and_sizes(lib):
     assert lib.splat_abi_version() == 1
     # workspace size queries are pure host arithmetic
