@@ -200,12 +200,19 @@ __global__ void pack64_kernel(SceneConst sc, ViewConst vc, double* __restrict__ 
 #ifndef BIN_STAGE
 #define BIN_STAGE 16384
 #endif
-constexpr int kBinBlock = BIN_BLOCK;   // ranks per block (a histogram row)
+constexpr int kBinBlock = BIN_BLOCK;   // ranks per block (a histogram row) on large grids
 #ifndef BIN_THREADS
 #define BIN_THREADS 1024
 #endif
 constexpr int kBinThreads = BIN_THREADS;   // kBinBlock / kBinThreads ranks per thread
 constexpr int kBinRPT = kBinBlock / kBinThreads;
+// Small grids bin in half-size blocks: a block's (block, tile) runs are then half as long, and
+// the fill's per-entry rank count within its run (quadratic in the run length) shrinks 4x,
+// while the per-block tile tables stay small (C5, 510 tiles: fill 72 -> 52 us; C3, 2040
+// tiles, keeps 4096: 2048 there costs 4.6 us of extra table work per view).
+constexpr int kBinSmallGridTiles = 1024;
+static_assert(kBinRPT >= 2 && kBinRPT % 2 == 0, "small grids use half-size blocks");
+__host__ __device__ constexpr int bin_rpt(int ntiles) { return ntiles < kBinSmallGridTiles ? kBinRPT / 2 : kBinRPT; }
 constexpr int kBinStage = BIN_STAGE;   // staged pairs per pass of the fill (2 CTAs/SM fit)
 constexpr int kColGroup = 16;        // rows per column-scan group
 constexpr int kBinSmemMax = 200 * 1024;
@@ -248,17 +255,19 @@ __device__ __forceinline__ BinRect bin_rect(int64_t n, int64_t r, const short4* 
     return q;
 }
 
+template <int RPT>
 __global__ void __launch_bounds__(kBinThreads) count_rows_kernel(int64_t n, const short4* __restrict__ bboxes,
                                                                  const uint32_t* __restrict__ touched, int ntx,
                                                                  int ntiles, uint32_t* __restrict__ hist) {
     extern __shared__ uint32_t h[];
-    const int64_t nblk = (n + kBinBlock - 1) / kBinBlock;
+    constexpr int64_t kBlk = (int64_t)RPT * kBinThreads;
+    const int64_t nblk = (n + kBlk - 1) / kBlk;
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         for (int t = threadIdx.x; t < ntiles; t += blockDim.x) h[t] = 0;
         __syncthreads();
 #pragma unroll
-        for (int j = 0; j < kBinRPT; ++j) {
-            const BinRect q = bin_rect(n, blk * kBinBlock + j * kBinThreads + threadIdx.x, bboxes, touched);
+        for (int j = 0; j < RPT; ++j) {
+            const BinRect q = bin_rect(n, blk * kBlk + j * kBinThreads + threadIdx.x, bboxes, touched);
             for (int ty = q.ty0; ty <= q.ty1; ++ty)
                 for (int tx = q.tx0; tx <= q.tx1; ++tx) atomicAdd(&h[ty * ntx + tx], 1u);
         }
@@ -391,6 +400,7 @@ __global__ void __launch_bounds__(1024) colscan_groups_scan_kernel(int ntiles, i
     if (threadIdx.x == 0) counters[0] = total;
 }
 
+template <int RPT>
 __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
     int64_t n, const short4* __restrict__ bboxes, const uint32_t* __restrict__ touched, int ntx, int ntiles,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ pre, const uint32_t* __restrict__ part,
@@ -407,13 +417,14 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
     uint16_t* stile = (uint16_t*)(stage + kBinStage);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
         write_range(t, tile_start, tile_count, ranges, cap);
-    const int64_t nblk = (n + kBinBlock - 1) / kBinBlock;
+    constexpr int64_t kBlk = (int64_t)RPT * kBinThreads;
+    const int64_t nblk = (n + kBlk - 1) / kBlk;
     const float inv_ntx = 1.0f / (float)ntx;
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-        short4 bb[kBinRPT];
+        short4 bb[RPT];
 #pragma unroll
-        for (int j = 0; j < kBinRPT; ++j)
-            bb[j] = bin_box(n, blk * kBinBlock + j * kBinThreads + threadIdx.x, bboxes, touched);
+        for (int j = 0; j < RPT; ++j)
+            bb[j] = bin_box(n, blk * kBlk + j * kBinThreads + threadIdx.x, bboxes, touched);
         // this block's tile histogram is count_rows' row (no second counting pass)
         const uint32_t* crow = hist + (size_t)blk * ntiles;
         for (int t = threadIdx.x; t < ntiles; t += blockDim.x) loff[t] = crow[t];
@@ -429,7 +440,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
                 if (threadIdx.x == 0) pass_end = ntiles;
             } else if (threadIdx.x == 0) {
                 // largest t1 whose tiles [t0, t1) hold <= kBinStage pairs; a single
-                // tile holds <= kBinBlock pairs of a block, so t1 > t0
+                // tile holds <= kBlk pairs of a block, so t1 > t0
                 int lo = t0 + 1, hi = ntiles;
                 const uint32_t lim = loff[t0] + kBinStage;
                 while (lo < hi) {
@@ -446,8 +457,8 @@ __global__ void __launch_bounds__(kBinThreads, 2) fill_rows_kernel(
             const uint32_t s1 = t1 < ntiles ? loff[t1] : total;
             __syncthreads();   // everyone has read loff[t0], loff[t1] before the cursors move
 #pragma unroll
-            for (int j = 0; j < kBinRPT; ++j) {
-                const uint32_t r = (uint32_t)(blk * kBinBlock + j * kBinThreads + threadIdx.x);
+            for (int j = 0; j < RPT; ++j) {
+                const uint32_t r = (uint32_t)(blk * kBlk + j * kBinThreads + threadIdx.x);
                 for (int ty = bb[j].z >> 4; ty <= (bb[j].w - 1) >> 4; ++ty) {
                     const int row = ty * ntx;
                     for (int tx = bb[j].x >> 4; tx <= (bb[j].y - 1) >> 4; ++tx) {
@@ -732,7 +743,8 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap) {
     L.tile_start = o; o = align_up(o + (size_t)L.ntx * L.nty * 4 + 4);
     L.cursor = o; o = align_up(o + (size_t)L.ntx * L.nty * 4);
     {
-        const size_t rows = (size_t)(nn + kBinBlock - 1) / kBinBlock;
+        const size_t blk = (size_t)bin_rpt(L.ntx * L.nty) * kBinThreads;
+        const size_t rows = (size_t)(nn + blk - 1) / blk;
         const size_t groups = (rows + kColGroup - 1) / kColGroup;
         L.bin_hist = o; o = align_up(o + rows * L.ntx * L.nty * 4);
         L.bin_pre = o; o = align_up(o + rows * L.ntx * L.nty * 4);
@@ -856,7 +868,9 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
     uint32_t* ranks = (uint32_t*)(ws + L.vals0);
     uint32_t* keys = (flags & SPLAT_BIN_KEYS) ? (uint32_t*)(ws + L.keys0) : nullptr;
     uint32_t* scan_tmp = (uint32_t*)(ws + L.tile_scan);
-    const int64_t nrows = (L.n + kBinBlock - 1) / kBinBlock;
+    const int rpt = bin_rpt(ntiles);
+    const int64_t bin_blk = (int64_t)rpt * kBinThreads;
+    const int64_t nrows = (L.n + bin_blk - 1) / bin_blk;
     const int ngroups = (int)((nrows + kColGroup - 1) / kColGroup);
     const int fill_smem = 8 * ntiles + 6 * kBinStage;
     const bool staged = ntiles <= 65535 && fill_smem <= kBinSmemMax && L.cap < 0xffffffffLL &&
@@ -865,10 +879,14 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         static PerDevice<bool> configured;
         bool ok = false;
         const int rc = configured.get(ok, [](bool& v) {
-            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(count_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  kBinSmemMax));
-            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fill_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  kBinSmemMax));
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(count_rows_kernel<kBinRPT>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmemMax));
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fill_rows_kernel<kBinRPT>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmemMax));
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(count_rows_kernel<kBinRPT / 2>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmemMax));
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fill_rows_kernel<kBinRPT / 2>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmemMax));
             SPLAT_CUDA_CHECK(cudaFuncSetAttribute(colscan_groups_scan_kernel,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kScanTilesMax * 4));
             v = true;
@@ -879,7 +897,12 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         uint32_t* pre = (uint32_t*)(ws + L.bin_pre);
         uint32_t* part = (uint32_t*)(ws + L.bin_part);
         const int grid = (int)(nrows < 148 * 2 ? nrows : 148 * 2);
-        count_rows_kernel<<<grid, kBinThreads, ntiles * 4, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist);
+        if (rpt == kBinRPT)
+            count_rows_kernel<kBinRPT><<<grid, kBinThreads, ntiles * 4, stream>>>(L.n, bboxes, touched, L.ntx, ntiles,
+                                                                                hist);
+        else
+            count_rows_kernel<kBinRPT / 2><<<grid, kBinThreads, ntiles * 4, stream>>>(L.n, bboxes, touched, L.ntx,
+                                                                                    ntiles, hist);
         note_launch();
         colscan_rows_kernel<<<dim3(ceil_div(ntiles, 128), ngroups), 128, 0, stream>>>(ntiles, (int)nrows, hist,
                                                                                      pre, part);
@@ -898,7 +921,8 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
             SPLAT_CUDA_CHECK(cudaGetLastError());
             return SPLAT_OK;
         }
-        fill_rows_kernel<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, pre, part,
+        auto fill = rpt == kBinRPT ? fill_rows_kernel<kBinRPT> : fill_rows_kernel<kBinRPT / 2>;
+        fill<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, pre, part,
                                                                   tile_start, tile_count, ranges, L.cap, ranks,
                                                                   keys, counters, (const uint32_t*)(ws + L.offsets),
                                                                   with_offsets ? (uint32_t*)(ws + L.slot_pos) : nullptr,
