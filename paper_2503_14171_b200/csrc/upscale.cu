@@ -878,6 +878,7 @@ __global__ void __launch_bounds__(256) upscale_bwd_kernel(const float* __restric
 // source pixel per thread contracts 8 rows of those.
 constexpr int kB4Cols = 32, kB4Rows = 8;
 constexpr int kB4WinC = 4 * kB4Cols + 8, kB4WinR = 4 * kB4Rows + 8;
+constexpr size_t kB4Smem = sizeof(float) * (8 * 2 * kB4WinC * 3 + kB4WinR * kB4Cols * 6);
 
 __device__ __forceinline__ void x4_weights(int j, int x, int n, float& wv, float& ws) {
     if (j < 4) {   // x = corner b of cell x-1, phase j
@@ -899,33 +900,63 @@ __device__ __forceinline__ void x4_weights(int j, int x, int n, float& wv, float
 
 __global__ void __launch_bounds__(256) upscale_bwd_x4_kernel(const float* __restrict__ adj,
                                                              float* __restrict__ dsrc, int in_w, int in_h) {
-    __shared__ float s_row[8][kB4WinC * 3];
-    __shared__ float s_g[kB4WinR][kB4Cols][6];
+    extern __shared__ __align__(16) unsigned char b4_smem[];
+    auto& s_row = *reinterpret_cast<float(*)[8][2][kB4WinC * 3]>(b4_smem);   // per warp, double-buffered
+    auto& s_g = *reinterpret_cast<float(*)[kB4WinR][kB4Cols][6]>(b4_smem + sizeof(float) * 8 * 2 * kB4WinC * 3);
     const int out_w = 4 * in_w, out_h = 4 * in_h;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int X0 = blockIdx.x * kB4Cols, Y0 = blockIdx.y * kB4Rows;
     const int u0 = 4 * X0 - 2, v0 = 4 * Y0 - 2;
     const int x = X0 + lane;
+    // adjoint row vi of the window (zero outside the image) -> buffer k of this warp, by cp.async
+    auto load_row = [&](int vi, int k) {
+        const int v = v0 + vi;
+        const bool vok = v >= 0 && v < out_h;
+        float* row = s_row[warp][k];
+        for (int e = lane; e < kB4WinC * 3; e += 32) {
+            const int u = u0 + e / 3;
+            const bool ok = vok && u >= 0 && u < out_w;
+            const float* src = ok ? adj + ((size_t)v * out_w + u0) * 3 + e : adj;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(row + e)), "l"(src),
+                         "r"(ok ? 4 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     float wv[8], ws[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) x4_weights(j, x, in_w, wv[j], ws[j]);
-    for (int vi = warp; vi < kB4WinR; vi += 8) {
-        const int v = v0 + vi;
-        float* row = s_row[warp];
-        const bool vok = v >= 0 && v < out_h;
-        for (int e = lane; e < kB4WinC * 3; e += 32) {
-            const int u = u0 + e / 3;
-            row[e] = (vok && u >= 0 && u < out_w) ? __ldg(adj + ((size_t)v * out_w + u0) * 3 + e) : 0.f;
+    load_row(warp, 0);
+    for (int vi = warp, k = 0; vi < kB4WinR; vi += 8, k ^= 1) {
+        if (vi + 8 < kB4WinR) {   // the next row streams in while this one is contracted
+            load_row(vi + 8, k ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncwarp();
+        const float* row = s_row[warp][k];
         float a[3] = {0.f, 0.f, 0.f}, b[3] = {0.f, 0.f, 0.f};
+        // the lane's 8 output pixels x 3 channels = 24 floats from byte 48 * lane: six 16-byte
+        // loads, conflict-free per 8-lane phase (scalar loads at a 12-float lane stride: 4-way)
+        float gv[24];
+        {
+            const float4* g4 = reinterpret_cast<const float4*>(row + 12 * lane);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                const float4 t = g4[q];
+                gv[4 * q] = t.x;
+                gv[4 * q + 1] = t.y;
+                gv[4 * q + 2] = t.z;
+                gv[4 * q + 3] = t.w;
+            }
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const float* g = row + (4 * lane + j) * 3;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                a[c] = fmaf(wv[j], g[c], a[c]);
-                b[c] = fmaf(ws[j], g[c], b[c]);
+                a[c] = fmaf(wv[j], gv[3 * j + c], a[c]);
+                b[c] = fmaf(ws[j], gv[3 * j + c], b[c]);
             }
         }
 #pragma unroll
@@ -1199,7 +1230,16 @@ int upscale_backward_impl(const float* adj, int out_w, int out_h, float* dsrc, i
     size_t smem = (size_t)(max_u + max_v) * sizeof(AxisMap) + (size_t)max_v * kBwCols * 6 * 4;
     if (out_w == 4 * in_w && out_h == 4 * in_h) {   // the x4 training path (C5)
         dim3 g4(ceil_div(in_w, kB4Cols), ceil_div(in_h, kB4Rows));
-        upscale_bwd_x4_kernel<<<g4, 256, 0, stream>>>(adj, dsrc, in_w, in_h);
+        static PerDevice<bool> b4_configured;
+        bool b4ok = false;
+        const int b4rc = b4_configured.get(b4ok, [](bool& v) {
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(upscale_bwd_x4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)kB4Smem));
+            v = true;
+            return SPLAT_OK;
+        });
+        if (b4rc != SPLAT_OK) return b4rc;
+        upscale_bwd_x4_kernel<<<g4, 256, kB4Smem, stream>>>(adj, dsrc, in_w, in_h);
         note_launch();
         SPLAT_CUDA_CHECK(cudaGetLastError());
         return SPLAT_OK;
