@@ -307,10 +307,15 @@ __global__ void colscan_groups_kernel(int ntiles, int ngroups, uint32_t* __restr
     if (t == 0) counters[5] = 0;
     if (t >= ntiles) return;
     uint32_t run = 0;
-    for (int g = 0; g < ngroups; ++g) {
-        const uint32_t v = part[(size_t)g * ntiles + t];
-        part[(size_t)g * ntiles + t] = run;
-        run += v;
+    for (int g0 = 0; g0 < ngroups; g0 += 16) {   // 16 loads in flight, then the prefix
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = g0 + i < ngroups ? part[(size_t)(g0 + i) * ntiles + t] : 0u;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (g0 + i < ngroups) part[(size_t)(g0 + i) * ntiles + t] = run;
+            run += v[i];
+        }
     }
     tile_count[t] = run;
 }
@@ -372,6 +377,9 @@ __device__ __forceinline__ short4 bin_box(int64_t n, int64_t r, const short4* bb
 // list's start (and the pair count) — what colscan_groups_kernel plus a
 // multi-kernel device scan did, in one launch (grids up to kScanTilesMax tiles).
 constexpr int kScanTilesMax = 16384;
+// above this many (group, tile) column entries the single-CTA fused scan is the bottleneck
+// (C4: 46 groups x 5100 tiles took 29 us in one CTA)
+constexpr int64_t kFusedScanWork = 65536;
 __global__ void __launch_bounds__(1024) colscan_groups_scan_kernel(int ntiles, int ngroups, uint32_t* __restrict__ part,
                                                                    uint32_t* __restrict__ tile_count,
                                                                    uint32_t* __restrict__ tile_start,
@@ -394,6 +402,20 @@ __global__ void __launch_bounds__(1024) colscan_groups_scan_kernel(int ntiles, i
         tile_count[t] = run;
         s_cnt[t] = run;
     }
+    __syncthreads();
+    const uint32_t total = block_exclusive_scan(s_cnt, ntiles, wsum);
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) tile_start[t] = s_cnt[t];
+    if (threadIdx.x == 0) counters[0] = total;
+}
+
+// One CTA: exclusive scan of the tile totals into each list's start and the pair count
+// (the second half of colscan_groups_scan_kernel, after a multi-CTA colscan_groups_kernel).
+__global__ void __launch_bounds__(1024) tile_scan_kernel(int ntiles, const uint32_t* __restrict__ tile_count,
+                                                         uint32_t* __restrict__ tile_start,
+                                                         uint32_t* __restrict__ counters) {
+    extern __shared__ uint32_t s_cnt[];
+    __shared__ uint32_t wsum[33];
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_cnt[t] = tile_count[t];
     __syncthreads();
     const uint32_t total = block_exclusive_scan(s_cnt, ntiles, wsum);
     for (int t = threadIdx.x; t < ntiles; t += blockDim.x) tile_start[t] = s_cnt[t];
@@ -889,6 +911,8 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmemMax));
             SPLAT_CUDA_CHECK(cudaFuncSetAttribute(colscan_groups_scan_kernel,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kScanTilesMax * 4));
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(tile_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kScanTilesMax * 4));
             v = true;
             return SPLAT_OK;
         });
@@ -907,9 +931,15 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         colscan_rows_kernel<<<dim3(ceil_div(ntiles, 128), ngroups), 128, 0, stream>>>(ntiles, (int)nrows, hist,
                                                                                      pre, part);
         note_launch();
-        if (ntiles <= kScanTilesMax) {
+        if (ntiles <= kScanTilesMax && (int64_t)ngroups * ntiles <= kFusedScanWork) {
             colscan_groups_scan_kernel<<<1, 1024, ntiles * 4, stream>>>(ntiles, ngroups, part, tile_count,
                                                                         tile_start, counters);
+            note_launch();
+        } else if (ntiles <= kScanTilesMax) {   // many groups x tiles: the column prefixes over many CTAs
+            colscan_groups_kernel<<<ceil_div(ntiles, 128), 128, 0, stream>>>(ntiles, ngroups, part, tile_count,
+                                                                            counters);
+            note_launch();
+            tile_scan_kernel<<<1, 1024, ntiles * 4, stream>>>(ntiles, tile_count, tile_start, counters);
             note_launch();
         } else {
             colscan_groups_kernel<<<ceil_div(ntiles, 128), 128, 0, stream>>>(ntiles, ngroups, part, tile_count,
