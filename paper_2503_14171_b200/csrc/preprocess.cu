@@ -210,9 +210,16 @@ constexpr int kBinRPT = kBinBlock / kBinThreads;
 // the fill's per-entry rank count within its run (quadratic in the run length) shrinks 4x,
 // while the per-block tile tables stay small (C5, 510 tiles: fill 72 -> 52 us; C3, 2040
 // tiles, keeps 4096: 2048 there costs 4.6 us of extra table work per view).
+// Small scenes halve the blocks further until there is at least one block per SM (C2:
+// 200k splats were 49 blocks of 4096 for 148 SMs).
 constexpr int kBinSmallGridTiles = 1024;
-static_assert(kBinRPT >= 2 && kBinRPT % 2 == 0, "small grids use half-size blocks");
-__host__ __device__ constexpr int bin_rpt(int ntiles) { return ntiles < kBinSmallGridTiles ? kBinRPT / 2 : kBinRPT; }
+constexpr int64_t kBinMinBlocks = 148;
+static_assert(kBinRPT >= 4 && kBinRPT % 4 == 0, "block sizes kBinRPT, /2, /4 ranks per thread");
+static int bin_rpt(int ntiles, int64_t n) {
+    int r = ntiles < kBinSmallGridTiles ? kBinRPT / 2 : kBinRPT;
+    while (r > kBinRPT / 4 && (n + (int64_t)r * kBinThreads - 1) / ((int64_t)r * kBinThreads) < kBinMinBlocks) r /= 2;
+    return r;
+}
 constexpr int kBinStage = BIN_STAGE;   // staged pairs per pass of the fill (2 CTAs/SM fit)
 constexpr int kColGroup = 16;        // rows per column-scan group
 constexpr int kBinSmemMax = 200 * 1024;
@@ -765,7 +772,7 @@ FrameLayout frame_layout(int64_t n, int width, int height, int64_t cap) {
     L.tile_start = o; o = align_up(o + (size_t)L.ntx * L.nty * 4 + 4);
     L.cursor = o; o = align_up(o + (size_t)L.ntx * L.nty * 4);
     {
-        const size_t blk = (size_t)bin_rpt(L.ntx * L.nty) * kBinThreads;
+        const size_t blk = (size_t)bin_rpt(L.ntx * L.nty, n) * kBinThreads;
         const size_t rows = (size_t)(nn + blk - 1) / blk;
         const size_t groups = (rows + kColGroup - 1) / kColGroup;
         L.bin_hist = o; o = align_up(o + rows * L.ntx * L.nty * 4);
@@ -890,7 +897,7 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
     uint32_t* ranks = (uint32_t*)(ws + L.vals0);
     uint32_t* keys = (flags & SPLAT_BIN_KEYS) ? (uint32_t*)(ws + L.keys0) : nullptr;
     uint32_t* scan_tmp = (uint32_t*)(ws + L.tile_scan);
-    const int rpt = bin_rpt(ntiles);
+    const int rpt = bin_rpt(ntiles, L.n);
     const int64_t bin_blk = (int64_t)rpt * kBinThreads;
     const int64_t nrows = (L.n + bin_blk - 1) / bin_blk;
     const int ngroups = (int)((nrows + kColGroup - 1) / kColGroup);
@@ -909,6 +916,10 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmemMax));
             SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fill_rows_kernel<kBinRPT / 2>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmemMax));
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(count_rows_kernel<kBinRPT / 4>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmemMax));
+            SPLAT_CUDA_CHECK(cudaFuncSetAttribute(fill_rows_kernel<kBinRPT / 4>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmemMax));
             SPLAT_CUDA_CHECK(cudaFuncSetAttribute(colscan_groups_scan_kernel,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kScanTilesMax * 4));
             SPLAT_CUDA_CHECK(cudaFuncSetAttribute(tile_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -921,12 +932,10 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
         uint32_t* pre = (uint32_t*)(ws + L.bin_pre);
         uint32_t* part = (uint32_t*)(ws + L.bin_part);
         const int grid = (int)(nrows < 148 * 2 ? nrows : 148 * 2);
-        if (rpt == kBinRPT)
-            count_rows_kernel<kBinRPT><<<grid, kBinThreads, ntiles * 4, stream>>>(L.n, bboxes, touched, L.ntx, ntiles,
-                                                                                hist);
-        else
-            count_rows_kernel<kBinRPT / 2><<<grid, kBinThreads, ntiles * 4, stream>>>(L.n, bboxes, touched, L.ntx,
-                                                                                    ntiles, hist);
+        auto count = rpt == kBinRPT       ? count_rows_kernel<kBinRPT>
+                     : rpt == kBinRPT / 2 ? count_rows_kernel<kBinRPT / 2>
+                                          : count_rows_kernel<kBinRPT / 4>;
+        count<<<grid, kBinThreads, ntiles * 4, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist);
         note_launch();
         colscan_rows_kernel<<<dim3(ceil_div(ntiles, 128), ngroups), 128, 0, stream>>>(ntiles, (int)nrows, hist,
                                                                                      pre, part);
@@ -951,7 +960,9 @@ int launch_binning(const FrameLayout& L, char* ws, int flags, cudaStream_t strea
             SPLAT_CUDA_CHECK(cudaGetLastError());
             return SPLAT_OK;
         }
-        auto fill = rpt == kBinRPT ? fill_rows_kernel<kBinRPT> : fill_rows_kernel<kBinRPT / 2>;
+        auto fill = rpt == kBinRPT       ? fill_rows_kernel<kBinRPT>
+                    : rpt == kBinRPT / 2 ? fill_rows_kernel<kBinRPT / 2>
+                                         : fill_rows_kernel<kBinRPT / 4>;
         fill<<<grid, kBinThreads, fill_smem, stream>>>(L.n, bboxes, touched, L.ntx, ntiles, hist, pre, part,
                                                                   tile_start, tile_count, ranges, L.cap, ranks,
                                                                   keys, counters, (const uint32_t*)(ws + L.offsets),
