@@ -415,18 +415,23 @@ def _scale_case(cfg):
         v = random_views(c.views, c.width, c.height, seed=11)[7]      # as bench.py's batch
     elif cfg == "c4":
         v = stereo_views(1, c.width, c.height, seed=11)[1]            # right eye of frame 0
+    elif cfg == "c5":   # the 1920x1080 training canvas seen at 480x270 (a bench view)
+        sc = synthetic_scene(c.n, c.canvas_w, c.canvas_h, c.scale_range, seed=5)
+        v = random_views(8, c.canvas_w, c.canvas_h, seed=13)[5]
     else:
         v = None
     return c, sc, v
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
 def test_preprocess_and_binning_bitexact_at_config_scale(P, oracle, cfg):
     """Integer parity at full config size (north_star: tile keys, sort order and per-tile
     ranges bit-exact): the device's depth order, bboxes and validity (float64 expression
     trees with libdevice exp/sin/cos/log vs numpy's) and the whole tile CSR (offsets,
     ranks, tile keys) equal the oracle's prepare_scene / bin_tiles
-    (raster_forward.py:79-149) for C2, one C3 bench view and one C4 eye."""
+    (raster_forward.py:79-149) for C2, one C3 bench view, one C4 eye and one C5 view -- the
+    three binning block sizes (1024 ranks for C2's 200k splats, 2048 on C5's 510-tile grid,
+    4096 for C3 / C4) and both column-scan shapes (C4's many-group table)."""
     from paper_2503_14171_b200.scenes import view_scene
     c, sc, v = _scale_case(cfg)
     P.render_forward(sc, c.width, c.height, view=v)   # sizes the pair capacity for this scene
