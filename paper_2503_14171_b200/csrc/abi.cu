@@ -296,6 +296,9 @@ int splat_render_views(const void* scene_const, int64_t n, const splat_view_t* v
         return set_error(SPLAT_ERR_PARAMETER, "invalid view batch");
     if (!plan) return set_error(SPLAT_ERR_PARAMETER, "upscale plan required (splat_upscale_plan)");
     if (out_w < width || out_h < height) return set_error(SPLAT_ERR_SCALE, "output must be at least source size");
+    if (n > 0 && nviews > 0 && !scene_const) return set_error(SPLAT_ERR_PARAMETER, "scene constants required");
+    for (int i = 0; i < nviews; ++i)
+        if (!outs[i]) return set_error(SPLAT_ERR_PARAMETER, "null output frame in the batch");
     for (int k = 0; k < nslots && k < nviews; ++k) {
         const splat_slot_t& sl = slots[k];
         const FrameLayout L = frame_layout(n, width, height, sl.pair_capacity);
