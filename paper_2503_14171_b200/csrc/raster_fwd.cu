@@ -281,11 +281,35 @@ __device__ __forceinline__ void apply_candidate(int st, float al, float gax, flo
     }
 }
 
+// An undecidable candidate (its float32 footprint test inside the guard band) stops the pixel
+// and flags it for the exact float64 re-render of fixup_kernel, which decides every candidate
+// of the pixel exactly anyway -- instead of calling the float64 test from the blend loop.
+// Inference: ~600 instead of ~230 fix-up pixels per C3 view, but the loop drops from 96
+// registers + stack to 70 registers and 7 persistent CTAs per SM (raster 388 -> 346 us);
+// training: 96 -> 80 registers at 6 CTAs per SM (C5 raster 227 -> 191 us).
+#ifndef RASTER_UNSURE_TO_FIXUP
+#define RASTER_UNSURE_TO_FIXUP 1
+#endif
+#ifndef RASTER_UNSURE_TO_FIXUP_TRAIN
+#define RASTER_UNSURE_TO_FIXUP_TRAIN 1
+#endif
 template <bool TRAIN>
 __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF& g, const float4& col,
                                                 const uint32_t* rp, uint32_t j, float cx, float cy,
                                                 Blend<TRAIN>& s, bool& active, bool& flagged) {
     float al, gax, gay, gaxy, rel;
+#if RASTER_UNSURE_TO_FIXUP || RASTER_UNSURE_TO_FIXUP_TRAIN
+    if (TRAIN ? RASTER_UNSURE_TO_FIXUP_TRAIN : RASTER_UNSURE_TO_FIXUP) {
+        const int st = eval_fast<!TRAIN>(g, cx, cy, al, gax, gay, gaxy, rel);
+        if (st == kUnsure) {
+            active = false;
+            flagged = true;
+            return;
+        }
+        if (st != kCulled) apply_candidate<TRAIN>(st, al, gax, gay, gaxy, rel, col, j, s, active, flagged);
+        return;
+    }
+#endif
     const int st = decide_candidate<TRAIN>(p, g, rp, cx, cy, al, gax, gay, gaxy, rel);
     if (st != kCulled) apply_candidate<TRAIN>(st, al, gax, gay, gaxy, rel, col, j, s, active, flagged);
 }
@@ -300,7 +324,13 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 #define RASTER_STATS 0   // work counters for tools/raster_stats.py
 #endif
 #ifndef RASTER_MIN_BLOCKS
-#define RASTER_MIN_BLOCKS 5   // 5 x 128 threads x 96 registers (6: spills, slower)
+// inference: 7 x 128 threads x 70 registers, no spills, since an undecidable candidate hands its
+// pixel to the fix-up instead of calling the float64 test in the blend loop (with that call the
+// loop needed 96 registers and a stack frame: 5 CTAs per SM)
+#define RASTER_MIN_BLOCKS 7
+#endif
+#ifndef RASTER_MIN_BLOCKS_TRAIN
+#define RASTER_MIN_BLOCKS_TRAIN 6   // training (float64 state): 80 registers, no spills, 6 CTAs per SM
 #endif
 #ifndef RASTER_UNROLL
 #define RASTER_UNROLL 2   // inference blend steps per loop iteration
@@ -342,7 +372,8 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 }
 
 template <bool TRAIN>
-__global__ void __launch_bounds__(kRasterThreads, RASTER_MIN_BLOCKS) raster_fwd_kernel(RasterArgs p) {
+__global__ void __launch_bounds__(kRasterThreads, TRAIN ? RASTER_MIN_BLOCKS_TRAIN : RASTER_MIN_BLOCKS)
+    raster_fwd_kernel(RasterArgs p) {
     // per warp, double-buffered: chunk c+1 is fetched with cp.async (LDGSTS) while chunk c blends
     // 80-byte stride: the four groups' candidates of a step fall on different banks
     struct PackS {
