@@ -526,6 +526,9 @@ __global__ void chain_kernel(int64_t n, const int32_t* __restrict__ rank_of, con
 #ifndef BW2_WARPS
 #define BW2_WARPS 4
 #endif
+#ifndef BW2_EXACT
+#define BW2_EXACT eval_exact_inl   // inlined: no call frame in the replay loop (eval_exact: 296-byte stack, C5 -1.4%)
+#endif
 #ifndef BW2_UNROLL
 #define BW2_UNROLL 1   // candidate steps per loop iteration
 #endif
@@ -778,7 +781,7 @@ __global__ void __launch_bounds__(kBw2Threads, BW2_MIN_BLOCKS) raster_bwd2_kerne
                         int st = eval_fast(g, cx, cy, al, gax, gay, gaxy, rel);
                         if (st == kUnsure) {
                             double a64;
-                            st = eval_exact(p.sc, p.vc, p.bboxes, S.rank[warp][b][idx], px, py, &a64);
+                            st = BW2_EXACT(p.sc, p.vc, p.bboxes, S.rank[warp][b][idx], px, py, &a64);
                             if (st != kCulled) canonical_values(g, cx, cy, st, al, gax, gay, gaxy);
                         }
                         if (st != kCulled) {
