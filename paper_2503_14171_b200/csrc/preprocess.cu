@@ -85,7 +85,10 @@ __device__ __forceinline__ int64_t clip64(int64_t v, int64_t lo, int64_t hi) {
 #ifndef PRE_THREADS
 #define PRE_THREADS 64   // 64 x 46 registers fit beside a persistent raster CTA set (C3 1896 -> 1911 frames/s)
 #endif
-__global__ void __launch_bounds__(PRE_THREADS) preprocess_kernel(SceneConst sc, ViewConst vc, int width, int height,
+#ifndef PRE_MINB
+#define PRE_MINB 1
+#endif
+__global__ void __launch_bounds__(PRE_THREADS, PRE_MINB) preprocess_kernel(SceneConst sc, ViewConst vc, int width, int height,
                                   PackF* __restrict__ pack, short4* __restrict__ bboxes,
                                   uint32_t* __restrict__ touched) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

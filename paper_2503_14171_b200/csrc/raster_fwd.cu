@@ -333,7 +333,7 @@ __device__ __forceinline__ void blend_candidate(const RasterArgs& p, const PackF
 #define RASTER_MIN_BLOCKS_TRAIN 6   // training (float64 state): 80 registers, no spills, 6 CTAs per SM
 #endif
 #ifndef RASTER_UNROLL
-#define RASTER_UNROLL 2   // inference blend steps per loop iteration
+#define RASTER_UNROLL 3   // inference blend steps per loop iteration (at 7 CTAs/SM: 3 > 2 > 4 > 1)
 #endif
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
@@ -626,6 +626,9 @@ __global__ void __launch_bounds__(kRasterThreads, TRAIN ? RASTER_MIN_BLOCKS_TRAI
 #ifndef FIX_THREADS
 #define FIX_THREADS 512
 #endif
+#ifndef FIX_MINB_INF
+#define FIX_MINB_INF 16
+#endif
 #ifndef FIX_GRID
 #define FIX_GRID (148 * 2)
 #endif
@@ -633,7 +636,7 @@ template <bool TRAIN>
 struct FixShape {
     static constexpr int kSeg = TRAIN ? FIX_SEG : 512;
     static constexpr int kThreads = TRAIN ? FIX_THREADS : 64;
-    static constexpr int kMinBlocks = TRAIN ? 1 : 16;   // 16 x 64 threads: <= 64 registers
+    static constexpr int kMinBlocks = TRAIN ? 1 : FIX_MINB_INF;   // 16 x 64 threads: <= 64 registers
     static constexpr int kPer = kSeg / kThreads;
     static_assert(kPer <= 32 && kSeg % kThreads == 0, "candidates per thread fit the keep mask");
 };
