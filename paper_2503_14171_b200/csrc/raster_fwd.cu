@@ -613,30 +613,42 @@ __global__ void __launch_bounds__(kRasterThreads, TRAIN ? RASTER_MIN_BLOCKS_TRAI
 //      float64 accumulation `acc = acc + alpha * (1 - acc)` for the
 //      termination decision (_kernels.py:105-111) and the same float32 (or
 //      TRAIN float64) value recurrences as the main pass.
-// Launch shapes.  Inference: 64 threads at <= 64 registers and a 512-candidate
-// segment (23 KB), small enough to co-reside with the next view's persistent
-// raster (which leaves 4096 registers and ~110 KB of shared memory per SM), so
-// the latency-bound fix-up of view k overlaps the raster of view k+1 in the
-// multi-stream pipeline (C3: 1831 -> 1855 frames/s; the 512-thread shape
-// serialises because it cannot fit beside a raster CTA).  Training keeps the
-// wide shape: its float64 blend state would spill at 64 registers.
+// Launch shapes.  Inference: one warp at <= 64 registers and a 128-candidate segment
+// (6 KB), small enough to co-reside with the next view's persistent raster (7 CTAs per
+// SM leave 2816 registers and ~20 KB of shared memory), so the latency-bound fix-up of
+// view k overlaps the raster of view k+1 in the multi-stream pipeline without taking a
+// raster CTA slot.  Training keeps the wide shape: its float64 blend state would spill
+// at 64 registers.
 #ifndef FIX_SEG
 #define FIX_SEG 2048
 #endif
 #ifndef FIX_THREADS
 #define FIX_THREADS 512
 #endif
+// Inference shape: one warp per pixel, 128-candidate segments (6 KB of shared memory, 64
+// registers), so a fix-up CTA fits beside the 7 persistent raster CTAs of an SM (they leave
+// 2816 registers): the 64-thread shape blocked a raster CTA slot per resident fix-up CTA (C3
+// 2410 -> 2455 frames/s with this shape and 8 CTAs per SM in the grid).
 #ifndef FIX_MINB_INF
-#define FIX_MINB_INF 16
+#define FIX_MINB_INF 32
+#endif
+#ifndef FIX_THREADS_INF
+#define FIX_THREADS_INF 32
+#endif
+#ifndef FIX_SEG_INF
+#define FIX_SEG_INF 128
+#endif
+#ifndef FIX_GRID_INF
+#define FIX_GRID_INF (148 * 8)
 #endif
 #ifndef FIX_GRID
 #define FIX_GRID (148 * 2)
 #endif
 template <bool TRAIN>
 struct FixShape {
-    static constexpr int kSeg = TRAIN ? FIX_SEG : 512;
-    static constexpr int kThreads = TRAIN ? FIX_THREADS : 64;
-    static constexpr int kMinBlocks = TRAIN ? 1 : FIX_MINB_INF;   // 16 x 64 threads: <= 64 registers
+    static constexpr int kSeg = TRAIN ? FIX_SEG : FIX_SEG_INF;
+    static constexpr int kThreads = TRAIN ? FIX_THREADS : FIX_THREADS_INF;
+    static constexpr int kMinBlocks = TRAIN ? 1 : FIX_MINB_INF;   // 32 x 32 threads: <= 64 registers
     static constexpr int kPer = kSeg / kThreads;
     static_assert(kPer <= 32 && kSeg % kThreads == 0, "candidates per thread fit the keep mask");
 };
@@ -827,7 +839,8 @@ int launch_fixup(const SceneConst& sc, const ViewConst& vc, const FrameLayout& L
         fixup_kernel<true><<<FIX_GRID, FixShape<true>::kThreads, sizeof(FixShared<true>), stream>>>(a); note_launch();
     } else {
 #ifndef TIMING_SKIP_FIX
-        fixup_kernel<false><<<FIX_GRID, FixShape<false>::kThreads, sizeof(FixShared<false>), stream>>>(a); note_launch();
+        fixup_kernel<false><<<FIX_GRID_INF, FixShape<false>::kThreads, sizeof(FixShared<false>), stream>>>(a);
+        note_launch();
 #endif
     }
     SPLAT_CUDA_CHECK(cudaGetLastError());
